@@ -1,0 +1,341 @@
+"""Pins for the CPU oracle (-m "not gpu"): each checks the oracle against something other
+than itself — values the paper prints (tests/golden/), closed forms, invariants, brute force.
+Pin numbers P1..P18 follow DESIGN.md §3 / SURVEY.md §8(c).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from synth import images as S
+from golden_io import read_golden
+from reference_butterfly import Counter, forward8, inverse8
+
+rng = np.random.default_rng(1234)
+
+
+def golden_c0():
+    return np.array([[int(v) for v in row] for row in read_golden("c0_matrix.txt")])
+
+
+# ---------------------------------------------------------------- matrices (P1-P5, P16)
+
+def test_P1_c0_equals_displayed_matrix():
+    T = O.c0_matrix()
+    assert T.shape == (8, 8)
+    assert np.array_equal(T, golden_c0())
+    assert set(np.unique(T)) <= {-1, 0, 1}
+
+
+def test_round_half_away_matlab_convention():
+    assert O.round_half_away(0.5) == 1 and O.round_half_away(-0.5) == -1
+    assert O.round_half_away(2.5) == 3 and O.round_half_away(-2.5) == -3
+    assert O.round_half_away(1.49999) == 1
+    # no entry of 2C is near a tie (reading R2 is therefore moot for C0)
+    frac = np.abs(2 * O.dct_matrix()) % 1.0
+    assert np.min(np.abs(frac - 0.5)) > 0.05
+
+
+def test_P2_orthogonalizer_is_printed_diagonal():
+    T = O.c0_matrix()
+    G = T @ T.T
+    assert np.array_equal(G, np.diag([8, 6, 4, 6, 8, 6, 4, 6]))
+    expr = [row[0] for row in read_golden("s_diagonal.txt")]
+    printed = np.array([eval(e, {"sqrt": math.sqrt}) for e in expr])
+    S_ = O.orthogonalizer()
+    assert np.allclose(S_, np.diag(printed), atol=1e-14)
+
+
+def test_P3_proposed_is_orthogonal():
+    C = O.proposed_matrix()
+    assert np.abs(C @ C.T - np.eye(8)).max() <= 1e-12        # P:228 "(i) it is orthogonal"
+    assert np.abs(C.T @ C - np.eye(8)).max() <= 1e-12
+
+
+def test_c0_is_not_orthogonal_and_coarse():
+    T = O.c0_matrix().astype(float)
+    assert np.abs(np.linalg.inv(T) - T.T).max() > 0.5        # P:180-181 C0^-1 != C0^T
+    assert np.allclose(O.coarse_matrix(), 0.5 * T)
+
+
+def test_P4_frobenius_scale_0_3922():
+    printed = float(read_golden("frobenius_scale.txt")[0][0])
+    a = O.frobenius_optimal_scale()
+    assert round(a, 4) == printed
+    # independent check: 1-D minimisation of ||a C0 - C||_F by golden-section search
+    C, T = O.dct_matrix(), O.c0_matrix().astype(float)
+    f = lambda s: np.linalg.norm(s * T - C)
+    lo, hi = 0.0, 1.0
+    g = (math.sqrt(5) - 1) / 2
+    for _ in range(200):
+        m1, m2 = hi - g * (hi - lo), lo + g * (hi - lo)
+        if f(m1) < f(m2):
+            hi = m2
+        else:
+            lo = m1
+    assert abs((lo + hi) / 2 - a) < 1e-8
+
+
+def test_P5_table2_error_energy():
+    rows = read_golden("table2_error_energy.txt")
+    tab = {r[0]: [float(v) for v in r[1:]] for r in rows}
+    eps_p = O.transfer_error_energy(O.proposed_matrix())
+    eps_s = O.transfer_error_energy(O.sdct_matrix())
+    for m in (1, 2, 3, 5, 6, 7):
+        assert abs(eps_p[m] - tab[str(m)][3]) <= 0.01, (m, eps_p[m])   # Proposed column
+        assert abs(eps_s[m] - tab[str(m)][2]) <= 0.01, (m, eps_s[m])   # SDCT column
+    assert abs(eps_p[[1, 2, 3, 5, 6, 7]].sum() - tab["total"][3]) <= 0.03
+    assert abs(eps_s[[1, 2, 3, 5, 6, 7]].sum() - tab["total"][2]) <= 0.03
+    # m = 0, 4: transfer functions equal the DCT's
+    assert eps_p[0] < 1e-12 and eps_p[4] < 1e-12
+
+
+def test_P16_example_values():
+    assert abs(O.dct_matrix()[1, 0] - 0.5 * math.cos(math.pi / 16)) < 1e-15
+    assert round(O.dct_matrix()[1, 0], 6) == 0.490393
+    assert round(O.proposed_matrix()[1, 0], 6) == round(1 / math.sqrt(6), 6) == 0.408248
+    assert abs(O.psnr(1.0, 1) - 20 * math.log10(255)) < 1e-12
+    assert round(float(O.psnr(1.0, 1)), 4) == 48.1308
+    assert O.psnr(0.0, 64) == np.inf
+
+
+# ---------------------------------------------------------------- fast algorithm (P6)
+
+def test_P6_butterfly_equals_matrix_and_counts_22():
+    T = O.c0_matrix()
+    table1 = [int(v) for v in read_golden("table1_proposed.txt")[0]]
+    for e in np.eye(8, dtype=np.int64):
+        assert list(forward8(list(e), Counter())) == list(T @ e)
+        assert list(inverse8(list(e), Counter())) == list(T.T @ e)
+    for _ in range(10000):
+        x = rng.integers(-255, 256, size=8)
+        assert list(forward8(list(x), Counter())) == list(T @ x)
+        assert list(inverse8(list(x), Counter())) == list(T.T @ x)
+    k = Counter()
+    forward8(list(range(8)), k)
+    assert [k.adds, k.mults, k.shifts, k.adds + k.mults + k.shifts] == table1
+    k = Counter()
+    inverse8(list(range(8)), k)
+    assert k.adds == 22 and k.mults == 0 and k.shifts == 0
+
+
+# ---------------------------------------------------------------- zig-zag (P12)
+
+def test_P12_zigzag_matches_standard_table():
+    tab = np.array([[int(v) for v in row] for row in read_golden("jpeg_zigzag.txt")])
+    Z = O.zigzag_index()
+    assert np.array_equal(Z, tab)
+    assert sorted(Z.ravel().tolist()) == list(range(64))
+    assert O.zigzag_order()[:6] == [(0, 0), (0, 1), (1, 0), (2, 0), (1, 1), (0, 2)]
+    assert Z[0].tolist() == [0, 1, 5, 6, 14, 15, 27, 28]
+    kept5 = {tuple(c) for c in np.argwhere(O.zonal_mask(5))}
+    assert kept5 == {(0, 0), (0, 1), (1, 0), (2, 0), (1, 1)}
+    for r, s in [(1, 0), (3, 1), (6, 2), (10, 3), (15, 4), (21, 5), (28, 6), (36, 7)]:
+        M = O.zonal_mask(r)
+        ii, jj = np.indices((8, 8))
+        assert np.array_equal(M, ii + jj <= s)               # triangular r <-> full anti-diagonals
+        assert np.array_equal(M, M.T)
+    with pytest.raises(ValueError):
+        O.zonal_mask(0)
+    with pytest.raises(ValueError):
+        O.zonal_mask(65)
+
+
+# ---------------------------------------------------------------- 2-D transform
+
+def brute_forward(X, T):
+    """Y[k][l] = sum_a sum_b T[k][a] X[a][b] T[l][b] with Python loops."""
+    return [[sum(T[k][a] * X[a][b] * T[l][b] for a in range(8) for b in range(8))
+             for l in range(8)] for k in range(8)]
+
+
+def test_forward_int_brute_force_and_layout():
+    T = O.c0_matrix().tolist()
+    img = rng.integers(0, 256, size=(16, 24), dtype=np.uint8)
+    Y = O.forward_int(img)[0]
+    for by in range(2):
+        for bx in range(3):
+            X = img[8 * by:8 * by + 8, 8 * bx:8 * bx + 8].astype(int).tolist()
+            assert Y[8 * by:8 * by + 8, 8 * bx:8 * bx + 8].tolist() == brute_forward(X, T)
+
+
+def test_P11_range_extremes_and_constant_blocks():
+    full = np.full((8, 8), 255, dtype=np.uint8)
+    Y = O.forward_int(full)[0]
+    assert Y[0, 0] == 16320 and np.count_nonzero(Y) == 1
+    for v in (0, 1, 77, 255):
+        img = np.full((16, 16), v, dtype=np.uint8)
+        assert np.abs(O.reconstruct_zonal(img, 1) - v).max() < 1e-12   # r = 1 lossless on constants
+    # checkerboards / random extremes stay inside the statically derived int16 range
+    for _ in range(200):
+        X = rng.choice([0, 255], size=(8, 8)).astype(np.uint8)
+        Y = O.forward_int(X)
+        assert Y.min() >= -8160 and Y.max() <= 16320
+
+
+def test_P13_literal_float_vs_exact_integer():
+    img = S.corpus_c2(3, 64, 64)
+    Z = O.forward_scaled(img)
+    Y = O.forward_int(img)
+    d = np.array([8, 6, 4, 6, 8, 6, 4, 6], dtype=float)
+    scale = np.tile(1 / np.sqrt(np.outer(d, d)), (8, 8))
+    assert np.abs(Z - Y * scale).max() <= 1e-12 * max(1.0, np.abs(Z).max())
+
+
+def test_P7_dc_rows_equal_dct_and_r1_equals_dct():
+    C, Cd = O.proposed_matrix(), O.dct_matrix()
+    assert np.abs(C[[0, 4]] - Cd[[0, 4]]).max() < 1e-15
+    img = S.corpus_c2(3, 64, 64)
+    sp = O.compress_zonal_sse(img, 1)
+    sd = O.compress_zonal_sse(img, 1, Cd)
+    assert np.allclose(sp, sd, rtol=1e-12)
+    Zp, Zd = O.forward_scaled(img), O.forward_scaled(img, Cd)
+    B1, B2 = O.to_blocks(Zp), O.to_blocks(Zd)
+    for (i, j) in [(0, 0), (0, 4), (4, 0), (4, 4)]:
+        assert np.abs(B1[..., i, j] - B2[..., i, j]).max() < 1e-9
+
+
+def test_P8_r64_is_lossless():
+    img = S.corpus_c2(3, 64, 64)
+    rec = O.reconstruct_zonal(img, 64)
+    assert np.abs(rec - img).max() < 1e-9
+    R = O.reconstruct_zonal_exact(img, 64)
+    assert np.array_equal(R, 576 * img.astype(np.int64))
+    assert np.all(O.psnr(O.sse_per_image(img, np.rint(rec)), 64 * 64) == np.inf)
+
+
+def test_P9_parseval_exact_integer_identity():
+    img = S.corpus_c2(3, 64, 64)
+    d = np.array([8, 6, 4, 6, 8, 6, 4, 6])
+    W = 576 // np.outer(d, d)
+    Y = O.to_blocks(O.forward_int(img))
+    x = img.astype(np.int64)
+    for r in (1, 5, 10, 17, 36, 63, 64):
+        R = O.reconstruct_zonal_exact(img, r)
+        sse576 = ((576 * x - R) ** 2).reshape(3, -1).sum(1)
+        kept = (W * O.zonal_mask(r) * Y * Y).reshape(3, -1).sum(1)
+        assert np.array_equal(sse576, 576 * (576 * (x * x).reshape(3, -1).sum(1) - kept))
+        sse = O.compress_zonal_sse(img, r)
+        assert np.allclose(sse, sse576 / 576.0 ** 2, rtol=1e-10, atol=1e-9)
+        rec = O.reconstruct_zonal(img, r)
+        assert np.abs(rec - R / 576.0).max() < 1e-10
+
+
+def test_P10_sse_monotone_in_r():
+    img = S.corpus_c2(3, 64, 64)
+    prev = None
+    for r in range(1, 65):
+        s = O.compress_zonal_sse(img, r)
+        if prev is not None:
+            assert np.all(s <= prev + 1e-7)
+        prev = s
+    assert np.all(prev < 1e-12)
+
+
+def test_P15_impulse_responses_kronecker():
+    T = O.c0_matrix()
+    d = np.array([8, 6, 4, 6, 8, 6, 4, 6])
+    W = 576 // np.outer(d, d)
+    K = np.kron(T, T)                                       # vec_row(T X T^T) = (T (x) T) vec_row(X)
+    for r in (1, 3, 10, 36, 64):
+        G = K.T @ np.diag((W * O.zonal_mask(r)).ravel()) @ K   # 576 x_hat = G x
+        for p in range(64):
+            X = np.zeros((8, 8), dtype=np.uint8)
+            X[p // 8, p % 8] = 1
+            R = O.reconstruct_zonal_exact(X, r)[0]
+            assert np.array_equal(R.ravel(), G[:, p])
+            assert np.abs(O.reconstruct_zonal(X, r)[0].ravel() - G[:, p] / 576).max() < 1e-12
+
+
+def test_P17_pattern_blocks_closed_form():
+    T = O.c0_matrix()
+    d = np.array([8, 6, 4, 6, 8, 6, 4, 6])
+    img, I, J, A = S.pattern_image_from_rows(T, 64, 128, seed=5)
+    Y = O.to_blocks(O.forward_int(img))[0]
+    for by in range(I.shape[0]):
+        for bx in range(I.shape[1]):
+            i, j, a = I[by, bx], J[by, bx], A[by, bx]
+            exp = np.zeros((8, 8), dtype=np.int64)
+            exp[0, 0] += 8192
+            exp[i, j] += a * d[i] * d[j]
+            assert np.array_equal(Y[by, bx], exp)
+    zz = O.zigzag_index()
+    for r in (1, 3, 10, 36, 64):
+        want = sum(0 if zz[I[b], J[b]] < r else A[b] ** 2 * d[I[b]] * d[J[b]] for b in np.ndindex(I.shape))
+        got = O.compress_zonal_sse(img, r)[0]
+        assert abs(got - want) <= 1e-8 * max(1, want)
+
+
+# ---------------------------------------------------------------- quantiser (R10, P14, P18)
+
+def test_quantize_exact_ties_round_away():
+    d = np.array([8, 6, 4, 6, 8, 6, 4, 6])
+    # put Y on an exact tie at (0,0): Z = Y/8, Z/q = Y/128 -> Y = 64 is 0.5 exactly
+    for y, k in [(64, 1), (-64, -1), (63, 0), (-63, 0), (192, 2), (-192, -2), (65, 1)]:
+        Y = np.zeros((8, 8), dtype=np.int64)
+        Y[0, 0] = y
+        assert O.quantize_exact(Y, 16.0)[0, 0, 0] == k
+    # (2,2): dd = 16, Z/q = Y / 64; (1,1): dd = 36 -> Y / 96
+    Y = np.zeros((8, 8), dtype=np.int64)
+    Y[2, 2], Y[1, 1] = -32, 48
+    k = O.quantize_exact(Y, 16.0)[0]
+    assert k[2, 2] == -1 and k[1, 1] == 1
+    # non-integer step uses exact rational arithmetic
+    Y[0, 0] = 3
+    assert O.quantize_exact(Y, 0.75)[0, 0, 0] == 1   # 3/8/0.75 = 0.5 -> 1
+
+
+def test_P14_quantizer_exact_vs_decimal_brute_force():
+    """k = round_half_away(Y / (q sqrt(d_i d_j))) recomputed with 60-digit decimal arithmetic."""
+    from decimal import Decimal, ROUND_HALF_UP, getcontext
+    getcontext().prec = 60
+    d = [8, 6, 4, 6, 8, 6, 4, 6]
+    Ys = np.arange(-1500, 1501)
+    for q in (16.0, 0.75, 5.0):
+        for (i, j) in [(0, 0), (1, 1), (0, 1), (2, 3), (2, 2), (7, 5)]:
+            Y = np.zeros((len(Ys), 8, 8), dtype=np.int64)
+            Y[:, i, j] = Ys
+            img = O.from_blocks(Y[:, None, None])
+            k = O.to_blocks(O.quantize_exact(img, q))[:, 0, 0, i, j]
+            den = Decimal(q) * Decimal(d[i] * d[j]).sqrt()
+            for y, kk in zip(Ys.tolist(), k.tolist()):
+                want = int((Decimal(y) / den).quantize(Decimal(1), rounding=ROUND_HALF_UP))
+                assert kk == want, (q, i, j, y, kk, want)
+
+
+def test_P18_quant_constant_image_closed_form():
+    for v in range(256):
+        img = np.full((8, 16), v, dtype=np.uint8)
+        rec = O.reconstruct_quant(img, 16.0)
+        want = 2 * math.floor(v / 2 + 0.5)
+        assert np.abs(rec - want).max() < 1e-9
+        sse = O.compress_quant_sse(img, 16.0)[0]
+        assert abs(sse - (0 if v % 2 == 0 else 128)) < 1e-7
+
+
+def test_u8_rounding():
+    x = np.array([-3.2, 0.49, 0.5, 254.5, 255.2, 300.0, 12.5, 13.5])
+    assert O.round_u8(x).tolist() == [0, 0, 1, 255, 255, 255, 13, 14]
+
+
+# ---------------------------------------------------------------- metrics, edge cases
+
+def test_psnr_mean_and_edge_cases():
+    assert O.mean_psnr([1.0 * 64, 4.0 * 64], 64) == pytest.approx(
+        0.5 * (20 * math.log10(255) + 10 * math.log10(255 ** 2 / 4)))
+    empty = np.zeros((0, 8, 8), dtype=np.uint8)
+    assert O.forward_int(empty).shape == (0, 8, 8)
+    assert O.compress_zonal_sse(empty, 10).shape == (0,)
+    with pytest.raises(ValueError):
+        O.to_blocks(np.zeros((12, 16), dtype=np.uint8))
+
+
+def test_synth_generators_shapes_and_ranges():
+    a = S.image_c1(0)
+    assert a.shape == (512, 512) and a.dtype == np.uint8
+    assert np.array_equal(a, S.image_c1(0))
+    c = S.corpus_c2(6, 64, 64)
+    assert c.shape == (6, 64, 64)
+    assert len({c[i].tobytes() for i in range(6)}) == 6
+    assert 20 < a.std() < 80

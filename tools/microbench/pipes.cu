@@ -1,0 +1,110 @@
+// Pipe-throughput microbenchmark for the sm_100a instruction mix the ADCT kernels use.
+// Measures lane-ops/clk/SM for IADD3, LOP3, PRMT, IMAD, FADD, FFMA, FADD2 (f32x2),
+// FFMA2 and ALU/FMA mixes, plus the SM clock seen during the run.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o pipes pipes.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define ITERS 4096
+#define CH 8
+
+template <int OP>
+__global__ void __launch_bounds__(256) kern(uint32_t* out, uint32_t seed, unsigned long long* clk) {
+  uint32_t r[CH];
+  unsigned long long rr[CH];
+  uint32_t f[CH];
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    r[c] = seed * (threadIdx.x + 1 + c);
+    f[c] = r[c] ^ 0x3f800000u;
+    rr[c] = ((unsigned long long)r[c] << 32) | (r[c] ^ 0x3f800000u);
+  }
+  uint32_t k1 = seed ^ 0x1234u, k2 = seed ^ 0x4321u;
+  unsigned long long kk = ((unsigned long long)k1 << 32) | k2;
+  unsigned long long t0 = clock64();
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) {
+      if (OP == 0) asm volatile("add.s32 %0, %0, %1;" : "+r"(r[c]) : "r"(k1));
+      if (OP == 1) asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(r[c]) : "r"(k1), "r"(k2));
+      if (OP == 2) asm volatile("prmt.b32 %0, %0, %1, 0x5140;" : "+r"(r[c]) : "r"(k1));
+      if (OP == 3) asm volatile("mad.lo.s32 %0, %0, %1, %2;" : "+r"(r[c]) : "r"(k1), "r"(k2));
+      if (OP == 4) asm volatile("add.f32 %0, %0, %1;" : "+r"(r[c]) : "r"(k1));
+      if (OP == 5) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+r"(r[c]) : "r"(k1), "r"(k2));
+      if (OP == 6) asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(rr[c]) : "l"(kk));
+      if (OP == 7) asm volatile("fma.rn.f32x2 %0, %0, %1, %0;" : "+l"(rr[c]) : "l"(kk));
+      if (OP == 8) {  // IADD3 + FADD2 interleaved
+        asm volatile("add.s32 %0, %0, %1;" : "+r"(r[c]) : "r"(k1));
+        asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(rr[c]) : "l"(kk));
+      }
+      if (OP == 9) {  // IADD3 + FADD interleaved
+        asm volatile("add.s32 %0, %0, %1;" : "+r"(r[c]) : "r"(k1));
+        asm volatile("add.f32 %0, %0, %1;" : "+r"(f[c]) : "r"(k1));
+      }
+      if (OP == 10) {  // 3-input integer add (IADD3 with three live operands)
+        asm volatile("{.reg .s32 t; add.s32 t, %0, %1; add.s32 %0, t, %2;}" : "+r"(r[c]) : "r"(k1), "r"(k2));
+      }
+      if (OP == 11) asm volatile("mad.wide.s32 %0, %1, %1, %0;" : "+l"(rr[c]) : "r"(r[c]));
+      if (OP == 12) asm volatile("add.f32 %0, %0, 0f3F800000;" : "+r"(r[c]));
+      if (OP == 13) asm volatile("fma.rn.f32 %0, %0, 0f3F800001, 0f3F800000;" : "+r"(r[c]));
+    }
+  }
+  unsigned long long t1 = clock64();
+  uint32_t acc = 0;
+#pragma unroll
+  for (int c = 0; c < CH; ++c) acc ^= r[c] ^ f[c] ^ (uint32_t)rr[c] ^ (uint32_t)(rr[c] >> 32);
+  out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  if (threadIdx.x == 0 && blockIdx.x == 0) *clk = t1 - t0;
+}
+
+template <int OP>
+void run(const char* name, int lanes_per_instr, int instr_per_chain_step, int sms) {
+  uint32_t* out;
+  unsigned long long* clk;
+  cudaMalloc(&out, 148 * 64 * 256 * 4);
+  cudaMalloc(&clk, 8);
+  int blocks = sms * 8;
+  kern<OP><<<blocks, 256>>>(out, 7, clk);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  kern<OP><<<blocks, 256>>>(out, 7, clk);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  unsigned long long cyc;
+  cudaMemcpy(&cyc, clk, 8, cudaMemcpyDeviceToHost);
+  double instrs = (double)blocks * 256 * ITERS * CH * instr_per_chain_step;
+  double ghz = cyc / (ms * 1e6);  // block-0 cycles over wall time (approx SM clock)
+  double lane_ops_per_clk_sm = instrs * lanes_per_instr / (ms * 1e-3) / (ghz * 1e9) / sms;
+  printf("%-14s %8.3f ms  clk~%.3f GHz  warp-instr/clk/SM=%.2f  lane-ops/clk/SM=%.1f\n", name, ms, ghz,
+         instrs / 32 / (ms * 1e-3) / (ghz * 1e9) / sms, lane_ops_per_clk_sm);
+  cudaError_t e = cudaGetLastError();
+  if (e) printf("err %s\n", cudaGetErrorString(e));
+  cudaFree(out);
+  cudaFree(clk);
+}
+
+int main() {
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  printf("SMs=%d\n", sms);
+  run<0>("iadd", 1, 1, sms);
+  run<10>("iadd3(2 ops)", 1, 2, sms);
+  run<1>("lop3", 1, 1, sms);
+  run<2>("prmt", 1, 1, sms);
+  run<3>("imad", 1, 1, sms);
+  run<11>("imad.wide", 1, 1, sms);
+  run<4>("fadd", 1, 1, sms);
+  run<12>("fadd-imm", 1, 1, sms);
+  run<5>("ffma", 1, 1, sms);
+  run<13>("ffma-imm", 1, 1, sms);
+  run<6>("fadd2", 2, 1, sms);
+  run<7>("ffma2", 2, 1, sms);
+  run<8>("iadd+fadd2", 1, 2, sms);
+  run<9>("iadd+fadd", 1, 2, sms);
+  return 0;
+}
