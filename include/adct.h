@@ -1,0 +1,149 @@
+/*
+ * adct.h — C ABI of the B200 (sm_100a) hot path of arXiv 1402.6034,
+ * "An orthogonal 8-point DCT approximation" (round-off approximation C0 = [2C],
+ * orthogonalised by the diagonal S).
+ *
+ * Citations: P:n = PAPER.md line n (Section / equation named beside it).
+ *
+ * Notation:
+ *   X    8x8 uint8 block, rows i (vertical), columns j (horizontal)
+ *   T    = C0 = [2 C], the displayed {0,+-1} matrix
+ *   d    = diag(T T^T) = (8,6,4,6,8,6,4,6); S = D = diag(d)^(-1/2)
+ *   C    = S . C0, the proposed orthogonal approximation C_orth
+ *   Y    = T . X . T^T, the integer coefficient block (22-addition butterfly    (P:250-283,
+ *          per 1-D transform, Table 1), |Y| <= 16320 so int16 is exact          P:482-487)
+ *   Z    = C . X . C^T = D . Y . D, Z_ij = Y_ij / sqrt(d_i d_j) (orthonormal domain)
+ *   M_r  keep the first r coefficients of the standard zig-zag scan (1<=r<=64)
+ *   X^   = C^T . (M_r . Z) . C, the reconstruction ("inverse procedure")
+ *   S is folded into the zonal / quantisation step: the kernels use the
+ *   integer weights W_ij = 576 / (d_i d_j) in {9,12,16,18,24,36}, so that
+ *   576 X^ = T^T (W . M_r . Y) T is an exact integer.
+ *   PSNR = 10 log10(255^2 / MSE), MSE = SSE / (h w)
+ *
+ * Layout (all entry points): n images of h x w pixels (h, w positive multiples of 8),
+ * row-major; `pitch` = bytes between rows; `img_stride` = bytes between images.
+ * Coefficient planes are image-shaped: coefficient (i, j) of the block at block
+ * row by, block column bx is stored at pixel (8 by + i, 8 bx + j) (reading R12).
+ *
+ * Ownership: every pointer is a DEVICE pointer owned by the caller unless stated;
+ * the library allocates nothing and keeps no mutable global state. All calls are
+ * asynchronous on `stream` (a cudaStream_t; NULL = legacy default stream); results
+ * are valid once the stream is synchronised. Functions are re-entrant.
+ *
+ * Errors: arguments are validated before anything is enqueued. On ADCT_EINVAL /
+ * ADCT_EALIGN nothing is enqueued. ADCT_ECUDA means a CUDA launch/driver error;
+ * adct_last_cuda_error() returns its cudaError_t (thread-local).
+ */
+#ifndef ADCT_H
+#define ADCT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* adct_stream_t; /* = cudaStream_t */
+
+typedef enum {
+  ADCT_OK = 0,
+  ADCT_EINVAL = 1, /* n < 1, h or w not a positive multiple of 8, r outside [1,64], q < 0 or NaN,
+                      pitch < row bytes, img_stride < h * pitch, unknown enum, NULL required pointer */
+  ADCT_EALIGN = 2, /* a pointer not 16-byte aligned, or a pitch / image stride not a multiple of 16
+                      (TMA global-address and stride rules) */
+  ADCT_ECUDA = 3   /* CUDA launch or driver error; see adct_last_cuda_error() */
+} adct_status;
+
+typedef enum {
+  ADCT_COEF_I16 = 0, /* int16 Y = T X T^T, exact (range [-8160, 16320])            */
+  ADCT_COEF_I32 = 1, /* int32 Y = T X T^T, exact                                     */
+  ADCT_COEF_F32 = 2  /* float Z = D Y D = C X C^T, one rounding: Y * fp32(1/sqrt(d_i d_j)) */
+} adct_coef_t;
+
+typedef enum {
+  ADCT_RECON_NONE = 0, /* no reconstruction written                                    */
+  ADCT_RECON_F32 = 1,  /* float X^ (unrounded, unclamped)                               */
+  ADCT_RECON_U8 = 2    /* uint8 clamp(round_half_away(X^), 0, 255), decided on the exact 576 X^ */
+} adct_recon_t;
+
+/*
+ * adct_forward — per 8x8 block, the 2-D forward transform T . X . T^T with the fast
+ * algorithm of Fig. 1 / Table 1 on rows then columns; zig-zag
+ * positions >= r are written as 0 (r = 64 keeps all).
+ *   src   [n][h][pitch] uint8, 16-B aligned; pitch, img_stride multiples of 16.
+ *   coef  image-shaped plane of coef_t; coef_pitch / coef_img_stride in bytes,
+ *         multiples of 16, coef_pitch >= w * sizeof(element).
+ * Returns ADCT_OK / EINVAL / EALIGN / ECUDA.
+ */
+adct_status adct_forward(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                         int64_t img_stride, int r, void* coef, adct_coef_t coef_t,
+                         int64_t coef_pitch, int64_t coef_img_stride, adct_stream_t stream);
+
+/*
+ * adct_inverse — the inverse procedure: X^ = C^T (M_r . Z) C per block.
+ * From ADCT_COEF_I16 / I32 (Y) the diagonal is folded as W / 576 (exact integers until the
+ * final division); from ADCT_COEF_F32 (Z) the kernel computes T^T (M_r . Z . s) T in fp32.
+ *   coef  image-shaped coefficient plane (layout as adct_forward's output).
+ *   dst   image-shaped reconstruction, dst_t = ADCT_RECON_F32 or ADCT_RECON_U8.
+ */
+adct_status adct_inverse(const void* coef, adct_coef_t coef_t, int64_t n, int64_t h, int64_t w,
+                         int64_t coef_pitch, int64_t coef_img_stride, int r, void* dst,
+                         adct_recon_t dst_t, int64_t dst_pitch, int64_t dst_img_stride,
+                         adct_stream_t stream);
+
+/*
+ * adct_compress_psnr — the fused hot path: forward (22-add butterflies, rows then columns),
+ * then either
+ *   q == 0: ZONAL — keep the first r zig-zag coefficients, S folded as W;
+ *   q  > 0: QUANT — D-scaled uniform quantiser on Z (reading R10): k = round_half_away(Z / q)
+ *           for zig-zag positions < r (else 0), dequantise Z^ = q k,
+ * then the inverse with C^T and the per-image squared error
+ * sse[i] = sum over image i of (x - X^)^2 on the unrounded reconstruction (reading R3).
+ *   src    [n][h][pitch] uint8 (as adct_forward).
+ *   recon  optional (may be NULL with recon_t = ADCT_RECON_NONE) image-shaped reconstruction.
+ *   sse    device double[n], OVERWRITTEN (the call zero-fills it on `stream` first).
+ * Quantiser decision: k = round-to-nearest(Y * c) in one fp32 FMA, c the smallest fp32 strictly
+ * above 1/(q sqrt(d_i d_j)); equal to the exact round-half-away decision for every reachable Y
+ * when q = 16 (exhaustive check: tests/test_quant_decision.py).
+ */
+adct_status adct_compress_psnr(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                               int64_t img_stride, int r, float q, void* recon,
+                               adct_recon_t recon_t, int64_t recon_pitch, int64_t recon_img_stride,
+                               double* sse, adct_stream_t stream);
+
+/*
+ * adct_psnr — PSNR = 10 log10(255^2 * pixels / sse[i]), +inf when sse[i] == 0.
+ *   sse, psnr  device double[count]; pixels = h * w of each image (> 0).
+ */
+adct_status adct_psnr(const double* sse, int64_t count, int64_t pixels, double* psnr,
+                      adct_stream_t stream);
+
+/*
+ * adct_compress_psnr_host — end-to-end entry with HOST buffers: copies the images from host
+ * memory (pinned recommended; host_src with host_pitch / host_img_stride in bytes) through the
+ * caller's device staging buffer `dev_buf` (dev_buf_bytes >= one image of h * w bytes; images are
+ * staged compactly, pitch = w rounded up to 16), runs adct_compress_psnr for each of the n_r
+ * values r_list[k] (q as above) and adct_psnr, and copies PSNR back to host_psnr[k * n + i].
+ *   dev_sse   device double[2 * n_r * n] scratch: SSE in [0, n_r n), PSNR in [n_r n, 2 n_r n).
+ *   Asynchronous: host_psnr is valid after `stream` is synchronised.
+ */
+adct_status adct_compress_psnr_host(const uint8_t* host_src, int64_t n, int64_t h, int64_t w,
+                                    int64_t host_pitch, int64_t host_img_stride,
+                                    const int* r_list, int n_r, float q, uint8_t* dev_buf,
+                                    int64_t dev_buf_bytes, double* dev_sse, double* host_psnr,
+                                    adct_stream_t stream);
+
+/* Human-readable status; static storage. */
+const char* adct_status_string(adct_status s);
+/* cudaError_t of the last ADCT_ECUDA on this thread (0 if none). */
+int adct_last_cuda_error(void);
+/* Library version (major * 10000 + minor * 100 + patch). */
+int adct_version(void);
+/* Number of kernel launches this library enqueued on this thread (bench instrumentation). */
+int64_t adct_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ADCT_H */

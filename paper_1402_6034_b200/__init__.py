@@ -1,0 +1,10 @@
+"""B200-native (sm_100a) hot path of arXiv 1402.6034: orthogonal round-off 8-point DCT approximation.
+
+Python surface = the C ABI in include/adct.h (same names, argument marshalling only):
+forward, inverse, compress_psnr, psnr, compress_psnr_host.  See DESIGN.md.
+"""
+from ._lib import (AdctError, compress_psnr, compress_psnr_host, empty_plane, forward, inverse,  # noqa: F401
+                   launch_count, load, psnr, to_device, version)
+
+__all__ = ["forward", "inverse", "compress_psnr", "psnr", "compress_psnr_host", "load", "launch_count",
+           "version", "AdctError", "empty_plane", "to_device"]

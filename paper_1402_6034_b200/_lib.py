@@ -1,0 +1,209 @@
+"""Thin ctypes binding over libadct.so (include/adct.h).
+
+Argument marshalling only: every step of the path runs in the library's sm_100a kernels.
+torch supplies device memory and the current CUDA stream.  There is no CPU fallback: if the
+library is missing or no CUDA device is present the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libadct.so")
+
+ADCT_OK, ADCT_EINVAL, ADCT_EALIGN, ADCT_ECUDA = 0, 1, 2, 3
+COEF = {"i16": 0, "i32": 1, "f32": 2}
+RECON = {None: 0, "none": 0, "f32": 1, "u8": 2}
+
+# exported symbols and their C signatures (checked by tests/test_abi_cpu.py against adct.h)
+_i64, _i32, _vp, _f32 = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_float
+SIGNATURES = {
+    "adct_forward": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _i32, _i64, _i64, _vp]),
+    "adct_inverse": (_i32, [_vp, _i32, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _i32, _i64, _i64, _vp]),
+    "adct_compress_psnr": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _f32, _vp, _i32, _i64, _i64,
+                                  _vp, _vp]),
+    "adct_psnr": (_i32, [_vp, _i64, _i64, _vp, _vp]),
+    "adct_compress_psnr_host": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _i32, _f32, _vp, _i64,
+                                       _vp, _vp, _vp]),
+    "adct_status_string": (ctypes.c_char_p, [_i32]),
+    "adct_last_cuda_error": (_i32, []),
+    "adct_version": (_i32, []),
+    "adct_launch_count": (_i64, []),
+}
+
+_lib = None
+
+
+class AdctError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        msg = load().adct_status_string(status).decode()
+        if status == ADCT_ECUDA:
+            msg += f" (cudaError {load().adct_last_cuda_error()})"
+        super().__init__(f"{where}: {msg}")
+
+
+def load():
+    """Load libadct.so (raises if it was not built: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing — run `python -m paper_1402_6034_b200.build`")
+        lib = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _check(st: int, where: str):
+    if st != ADCT_OK:
+        raise AdctError(st, where)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream(stream=None):
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _plane(t, elem: int):
+    """(ptr, n, h, w, pitch_bytes, img_stride_bytes) of a [n, h, w] CUDA tensor with unit column stride."""
+    if t.dim() == 2:
+        t = t.unsqueeze(0)
+    if t.dim() != 3:
+        raise ValueError("expected a [n, h, w] (or [h, w]) tensor")
+    if not t.is_cuda:
+        raise ValueError("tensor must be on a CUDA device (no CPU path)")
+    if t.stride(2) != 1:
+        raise ValueError("columns must be contiguous")
+    n, h, w = t.shape
+    return t.data_ptr(), n, h, w, t.stride(1) * elem, t.stride(0) * elem
+
+
+def empty_plane(n: int, h: int, w: int, dtype, device="cuda"):
+    """[n, h, w] tensor whose row pitch is padded to a multiple of 16 bytes (the ABI's TMA rule)."""
+    torch = _torch()
+    es = torch.empty((), dtype=dtype).element_size()
+    wp = -(-w * es // 16) * 16 // es
+    return torch.empty((n, h, wp), dtype=dtype, device=device)[:, :, :w]
+
+
+def to_device(x, device="cuda"):
+    """Copy a host uint8 [n, h, w] (or [h, w]) array into a 16-byte-pitched device plane."""
+    torch = _torch()
+    t = torch.as_tensor(np.ascontiguousarray(x) if isinstance(x, np.ndarray) else x)
+    if t.dim() == 2:
+        t = t.unsqueeze(0)
+    out = empty_plane(*t.shape, dtype=t.dtype, device=device)
+    out.copy_(t)
+    return out
+
+
+def launch_count() -> int:
+    return int(load().adct_launch_count())
+
+
+def version() -> int:
+    return int(load().adct_version())
+
+
+def forward(x, r: int = 64, coef: str = "i16", out=None, stream=None):
+    """adct_forward: Y = T X T^T per 8x8 block (i16 / i32) or Z = D Y D (f32), image-shaped."""
+    torch = _torch()
+    p, n, h, w, pitch, istr = _plane(x, 1)
+    dt = {"i16": torch.int16, "i32": torch.int32, "f32": torch.float32}[coef]
+    if out is None:
+        out = empty_plane(n, h, w, dt, x.device)
+    es = out.element_size()
+    q, *_rest = _plane(out, es)
+    _check(load().adct_forward(p, n, h, w, pitch, istr, r, q, COEF[coef], out.stride(-2) * es,
+                               out.stride(0) * es if out.dim() == 3 else h * out.stride(-2) * es,
+                               _stream(stream)), "adct_forward")
+    return out
+
+
+def inverse(coef, r: int = 64, out: str = "f32", dst=None, stream=None):
+    """adct_inverse: X^ = C^T (M_r . Z) C per block, from an image-shaped coefficient plane."""
+    torch = _torch()
+    kind = {torch.int16: "i16", torch.int32: "i32", torch.float32: "f32"}[coef.dtype]
+    p, n, h, w, pitch, istr = _plane(coef, coef.element_size())
+    if dst is None:
+        dst = empty_plane(n, h, w, torch.float32 if out == "f32" else torch.uint8, coef.device)
+    es = dst.element_size()
+    d, *_r = _plane(dst, es)
+    _check(load().adct_inverse(p, COEF[kind], n, h, w, pitch, istr, r, d, RECON[out], dst.stride(-2) * es,
+                               dst.stride(0) * es if dst.dim() == 3 else h * dst.stride(-2) * es,
+                               _stream(stream)), "adct_inverse")
+    return dst
+
+
+def compress_psnr(x, r: int, q: float = 0.0, recon: str | None = None, sse=None, recon_out=None,
+                  stream=None):
+    """adct_compress_psnr: fused forward + zonal (q = 0) / quantiser (q > 0) + inverse + per-image SSE.
+
+    Returns sse (float64 [n], device) or (sse, recon) when `recon` is "f32" / "u8".
+    """
+    torch = _torch()
+    p, n, h, w, pitch, istr = _plane(x, 1)
+    if sse is None:
+        sse = torch.empty((n,), dtype=torch.float64, device=x.device)
+    rp, rpitch, ristr = 0, 0, 0
+    if recon is not None and recon != "none":
+        if recon_out is None:
+            recon_out = empty_plane(n, h, w, torch.float32 if recon == "f32" else torch.uint8, x.device)
+        es = recon_out.element_size()
+        rp, _n, _h, _w, rpitch, ristr = _plane(recon_out, es)
+    _check(load().adct_compress_psnr(p, n, h, w, pitch, istr, r, float(q), rp, RECON[recon], rpitch, ristr,
+                                     sse.data_ptr(), _stream(stream)), "adct_compress_psnr")
+    return (sse, recon_out) if recon not in (None, "none") else sse
+
+
+def psnr(sse, pixels: int, out=None, stream=None):
+    """adct_psnr: 10 log10(255^2 pixels / sse), +inf where sse == 0 (device)."""
+    torch = _torch()
+    if out is None:
+        out = torch.empty_like(sse)
+    _check(load().adct_psnr(sse.data_ptr(), sse.numel(), pixels, out.data_ptr(), _stream(stream)), "adct_psnr")
+    return out
+
+
+def compress_psnr_host(host_images, r_list, q: float = 0.0, dev_buf=None, dev_sse=None, host_psnr=None,
+                       stream=None):
+    """adct_compress_psnr_host: end-to-end from host memory (pinned torch uint8 [n, h, w] or numpy).
+
+    Returns host PSNR [len(r_list), n] (float64, valid after the stream is synchronised).
+    """
+    torch = _torch()
+    if isinstance(host_images, np.ndarray):
+        host_images = torch.from_numpy(np.ascontiguousarray(host_images))
+    if host_images.dim() == 2:
+        host_images = host_images.unsqueeze(0)
+    n, h, w = host_images.shape
+    if host_images.is_cuda or host_images.stride(2) != 1:
+        raise ValueError("host_images must be a host tensor with contiguous columns")
+    dpitch = (w + 15) // 16 * 16
+    if dev_buf is None:
+        dev_buf = torch.empty((n * h * dpitch,), dtype=torch.uint8, device="cuda")
+    nr = len(r_list)
+    if dev_sse is None:
+        dev_sse = torch.empty((2 * nr * n,), dtype=torch.float64, device="cuda")
+    if host_psnr is None:
+        host_psnr = torch.empty((nr, n), dtype=torch.float64, pin_memory=True)
+    rl = (ctypes.c_int * nr)(*[int(v) for v in r_list])
+    _check(load().adct_compress_psnr_host(host_images.data_ptr(), n, h, w, host_images.stride(1),
+                                          host_images.stride(0), rl, nr, float(q), dev_buf.data_ptr(),
+                                          dev_buf.numel(), dev_sse.data_ptr(), host_psnr.data_ptr(),
+                                          _stream(stream)), "adct_compress_psnr_host")
+    return host_psnr

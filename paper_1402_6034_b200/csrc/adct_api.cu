@@ -1,0 +1,381 @@
+// adct_api.cu — host side of the C ABI (include/adct.h): validation, TMA descriptors,
+// per-call weight / quantiser tables, dispatch and launch.
+#include "adct.h"
+#include "adct_kernels.cuh"
+
+namespace adct {
+__global__ void __launch_bounds__(256) k_psnr(const double* __restrict__ sse, int64_t count, double pixels,
+                       double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const double s = sse[i];
+  out[i] = (s == 0.0) ? __longlong_as_double(0x7ff0000000000000ll)
+                      : 10.0 * log10(65025.0 * pixels / s);
+}
+}  // namespace adct
+
+// ==========================================================================================
+// Host side: validation, tensor maps, dispatch, C ABI
+// ==========================================================================================
+namespace {
+
+using namespace adct;
+
+thread_local int g_last_cuda = 0;
+thread_local int64_t g_launches = 0;
+
+adct_status cuda_fail(cudaError_t e) {
+  g_last_cuda = (int)e;
+  return ADCT_ECUDA;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;  // immutable after first resolution
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+adct_status make_u8_map(CUtensorMap* map, const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                        int64_t img_stride) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return cuda_fail(cudaErrorNotSupported);
+  cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)img_stride};
+  cuuint32_t box[3] = {TILE_W, TILE_H, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)src, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cuda_fail(cudaErrorInvalidValue);
+  return ADCT_OK;
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+adct_status check_geom(int64_t n, int64_t h, int64_t w) {
+  if (n < 1 || h < 8 || w < 8 || (h & 7) || (w & 7)) return ADCT_EINVAL;
+  if (n > INT32_MAX || h > INT32_MAX || w > INT32_MAX) return ADCT_EINVAL;
+  return ADCT_OK;
+}
+
+adct_status check_plane(const void* p, int64_t h, int64_t row_bytes, int64_t pitch, int64_t img_stride) {
+  if (!p) return ADCT_EINVAL;
+  if (pitch < row_bytes || img_stride < h * pitch) return ADCT_EINVAL;
+  if (!aligned16(p) || (pitch & 15) || (img_stride & 15)) return ADCT_EALIGN;
+  return ADCT_OK;
+}
+
+TileGeo make_geo(int64_t h, int64_t w) {
+  TileGeo g;
+  g.tiles_x = (w + TILE_W - 1) / TILE_W;
+  g.tiles_y = (h + TILE_H - 1) / TILE_H;
+  g.per_img = g.tiles_x * g.tiles_y;
+  return g;
+}
+
+constexpr int zz_host(int i, int j) { return zz_index(i, j); }
+double dd_host(int k, int l) { return (double)(dval(k) * dval(l)); }
+
+// Smallest fp32 strictly above the exact 1 / (q sqrt(dd)): ties of the half-away rounding
+// round away from zero (R10); compared exactly with 128-bit integers.
+float quant_recip(float q, int dd) {
+  auto above = [&](float c) {
+    // c > 1/(q sqrt dd)  <=>  (c q)^2 dd > 1, with c = mc 2^ec, q = mq 2^eq exactly
+    int ec, eq;
+    double fc = frexp((double)c, &ec), fq = frexp((double)q, &eq);
+    uint64_t mc = (uint64_t)ldexp(fc, 24), mq = (uint64_t)ldexp(fq, 24);
+    ec -= 24;
+    eq -= 24;
+    unsigned __int128 m = (unsigned __int128)(mc * mq);  // < 2^48
+    unsigned __int128 lhs = m * m * (unsigned __int128)dd;  // (c q)^2 dd = lhs * 2^(2(ec+eq))
+    int e = 2 * (ec + eq);                                 // compare lhs * 2^e > 1
+    if (e >= 0) return lhs > 0;
+    int sh = -e;
+    if (sh >= 127) return false;
+    return lhs > ((unsigned __int128)1 << sh);
+  };
+  float c = (float)(1.0 / ((double)q * sqrt((double)dd)));
+  while (above(nextafterf(c, 0.f))) c = nextafterf(c, 0.f);
+  while (!above(c)) c = nextafterf(c, INFINITY);
+  return c;
+}
+
+void fill_zonal_tables(Tables& t, int r) {
+  for (int k = 0; k < 8; ++k)
+    for (int l = 0; l < 8; ++l) {
+      const bool keep = zz_host(k, l) < r;
+      const float w = keep ? (float)wval(k, l) : 0.f;
+      t.w[k * 8 + l] = make_float2(w, w);
+      t.c[k * 8 + l] = make_float2(-KF * w, -KF * w);
+    }
+}
+
+void fill_quant_tables(Tables& t, int r, float q) {
+  for (int k = 0; k < 8; ++k)
+    for (int l = 0; l < 8; ++l) {
+      const bool keep = zz_host(k, l) < r;
+      // dequantised Z^ = q k enters the inverse as D Z^ D: q k / sqrt(d_k d_l) (x^ domain, fp32)
+      const float qw = keep ? (float)((double)q / sqrt(dd_host(k, l))) : 0.f;
+      const float c = quant_recip(q, dval(k) * dval(l));
+      t.w[k * 8 + l] = make_float2(qw, qw);
+      t.c[k * 8 + l] = make_float2(c, c);
+    }
+}
+
+template <class K, class P>
+adct_status launch_tma_kernel(K kern, const CUtensorMap& map, const P& params, int64_t tiles,
+                              cudaStream_t stream) {
+  const int smem = WARPS * STAGES * TILE_BYTES + WARPS * STAGES * 8;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return cuda_fail(e);
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, smem);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (occ < 1) occ = 1;
+  int64_t grid = (int64_t)sms * occ;
+  const int64_t need = (tiles + WARPS - 1) / WARPS;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, WARPS * 32, smem, stream>>>(map, params);
+  ++g_launches;
+  e = cudaGetLastError();
+  return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
+}
+
+
+}  // namespace
+
+extern "C" {
+
+const char* adct_status_string(adct_status s) {
+  switch (s) {
+    case ADCT_OK: return "ok";
+    case ADCT_EINVAL: return "invalid argument";
+    case ADCT_EALIGN: return "misaligned pointer, pitch or stride (16-byte rule)";
+    case ADCT_ECUDA: return "CUDA error";
+  }
+  return "unknown status";
+}
+
+int adct_last_cuda_error(void) { return g_last_cuda; }
+int adct_version(void) { return 10000; }
+int64_t adct_launch_count(void) { return g_launches; }
+
+adct_status adct_forward(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                         int64_t img_stride, int r, void* coef, adct_coef_t coef_t, int64_t coef_pitch,
+                         int64_t coef_img_stride, adct_stream_t stream) {
+  adct_status st = check_geom(n, h, w);
+  if (st) return st;
+  if (r < 1 || r > 64) return ADCT_EINVAL;
+  if (coef_t != ADCT_COEF_I16 && coef_t != ADCT_COEF_I32 && coef_t != ADCT_COEF_F32) return ADCT_EINVAL;
+  if ((st = check_plane(src, h, w, pitch, img_stride))) return st;
+  const int es = coef_t == ADCT_COEF_I16 ? 2 : 4;
+  if ((st = check_plane(coef, h, w * es, coef_pitch, coef_img_stride))) return st;
+  CUtensorMap map;
+  if ((st = make_u8_map(&map, src, n, h, w, pitch, img_stride))) return st;
+  ForwardParams p;
+  memset(&p, 0, sizeof(p));
+  p.geo = make_geo(h, w);
+  p.tiles = p.geo.per_img * n;
+  p.h = (int)h;
+  p.w = (int)w;
+  p.coef = (uint8_t*)coef;
+  p.coef_pitch = coef_pitch;
+  p.coef_img_stride = coef_img_stride;
+  p.masked = r < 64;
+  p.keep = (r >= 64) ? ~0ull : ((1ull << r) - 1ull);
+  for (int k = 0; k < 8; ++k)
+    for (int m = 0; m < 4; ++m) {
+      uint32_t mk = 0;
+      if (zz_host(k, 2 * m) < r) mk |= 0xFFFFu;
+      if (zz_host(k, 2 * m + 1) < r) mk |= 0xFFFF0000u;
+      p.m16[k * 4 + m] = mk;
+    }
+  for (int k = 0; k < 8; ++k)
+    for (int l = 0; l < 8; ++l)
+      p.sc[k * 8 + l] = (zz_host(k, l) < r) ? (float)(1.0 / sqrt(dd_host(k, l))) : 0.f;
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (coef_t) {
+    case ADCT_COEF_I16: return launch_tma_kernel(k_forward<OUT_I16>, map, p, p.tiles, s);
+    case ADCT_COEF_I32: return launch_tma_kernel(k_forward<OUT_I32>, map, p, p.tiles, s);
+    default: return launch_tma_kernel(k_forward<OUT_F32>, map, p, p.tiles, s);
+  }
+}
+
+adct_status adct_inverse(const void* coef, adct_coef_t coef_t, int64_t n, int64_t h, int64_t w,
+                         int64_t coef_pitch, int64_t coef_img_stride, int r, void* dst, adct_recon_t dst_t,
+                         int64_t dst_pitch, int64_t dst_img_stride, adct_stream_t stream) {
+  adct_status st = check_geom(n, h, w);
+  if (st) return st;
+  if (r < 1 || r > 64) return ADCT_EINVAL;
+  if (coef_t != ADCT_COEF_I16 && coef_t != ADCT_COEF_I32 && coef_t != ADCT_COEF_F32) return ADCT_EINVAL;
+  if (dst_t != ADCT_RECON_F32 && dst_t != ADCT_RECON_U8) return ADCT_EINVAL;
+  const int es = coef_t == ADCT_COEF_I16 ? 2 : 4;
+  if ((st = check_plane(coef, h, w * es, coef_pitch, coef_img_stride))) return st;
+  if ((st = check_plane(dst, h, w * (dst_t == ADCT_RECON_F32 ? 4 : 1), dst_pitch, dst_img_stride))) return st;
+  InverseParams p;
+  memset(&p, 0, sizeof(p));
+  p.geo = make_geo(h, w);
+  p.tiles = p.geo.per_img * n;
+  p.h = (int)h;
+  p.w = (int)w;
+  p.coef = (const uint8_t*)coef;
+  p.coef_pitch = coef_pitch;
+  p.coef_img_stride = coef_img_stride;
+  p.dst = (uint8_t*)dst;
+  p.dst_pitch = dst_pitch;
+  p.dst_img_stride = dst_img_stride;
+  for (int k = 0; k < 8; ++k)
+    for (int l = 0; l < 8; ++l) {
+      float m = 0.f;
+      if (zz_host(k, l) < r)
+        m = (coef_t == ADCT_COEF_F32) ? (float)(576.0 / sqrt(dd_host(k, l))) : (float)wval(k, l);
+      p.tab.w[k * 8 + l] = make_float2(m, m);
+    }
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t grid = (int64_t)sms * 3;
+  const int64_t need = (p.tiles + WARPS - 1) / WARPS;
+  if (grid > need) grid = need;
+  cudaStream_t s = (cudaStream_t)stream;
+#define ADCT_INV(IN, RC) k_inverse<IN, RC><<<(unsigned)grid, WARPS * 32, 0, s>>>(p)
+  if (coef_t == ADCT_COEF_I16) {
+    if (dst_t == ADCT_RECON_F32) ADCT_INV(OUT_I16, REC_F32); else ADCT_INV(OUT_I16, REC_U8);
+  } else if (coef_t == ADCT_COEF_I32) {
+    if (dst_t == ADCT_RECON_F32) ADCT_INV(OUT_I32, REC_F32); else ADCT_INV(OUT_I32, REC_U8);
+  } else {
+    if (dst_t == ADCT_RECON_F32) ADCT_INV(OUT_F32, REC_F32); else ADCT_INV(OUT_F32, REC_U8);
+  }
+#undef ADCT_INV
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
+}
+
+adct_status adct_compress_psnr(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                               int64_t img_stride, int r, float q, void* recon, adct_recon_t recon_t,
+                               int64_t recon_pitch, int64_t recon_img_stride, double* sse,
+                               adct_stream_t stream) {
+  adct_status st = check_geom(n, h, w);
+  if (st) return st;
+  if (r < 1 || r > 64 || !(q >= 0.f) || isinf(q)) return ADCT_EINVAL;
+  if (recon_t != ADCT_RECON_NONE && recon_t != ADCT_RECON_F32 && recon_t != ADCT_RECON_U8) return ADCT_EINVAL;
+  if (!sse) return ADCT_EINVAL;
+  if ((st = check_plane(src, h, w, pitch, img_stride))) return st;
+  if ((uintptr_t)sse & 7u) return ADCT_EALIGN;
+  if (recon_t != ADCT_RECON_NONE &&
+      (st = check_plane(recon, h, w * (recon_t == ADCT_RECON_F32 ? 4 : 1), recon_pitch, recon_img_stride)))
+    return st;
+  CUtensorMap map;
+  if ((st = make_u8_map(&map, src, n, h, w, pitch, img_stride))) return st;
+  CompressParams p;
+  memset(&p, 0, sizeof(p));
+  p.geo = make_geo(h, w);
+  p.tiles = p.geo.per_img * n;
+  p.h = (int)h;
+  p.w = (int)w;
+  p.sse = sse;
+  p.recon = (uint8_t*)recon;
+  p.recon_pitch = recon_pitch;
+  p.recon_img_stride = recon_img_stride;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(double) * (size_t)n, s);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (q > 0.f) {
+    fill_quant_tables(p.tab, r, q);
+    if (recon_t == ADCT_RECON_NONE) return launch_tma_kernel(k_compress<RT, MODE_QUANT, REC_NONE>, map, p, p.tiles, s);
+    if (recon_t == ADCT_RECON_F32) return launch_tma_kernel(k_compress<RT, MODE_QUANT, REC_F32>, map, p, p.tiles, s);
+    return launch_tma_kernel(k_compress<RT, MODE_QUANT, REC_U8>, map, p, p.tiles, s);
+  }
+  fill_zonal_tables(p.tab, r);
+  if (recon_t == ADCT_RECON_NONE) {
+    return launch_tma_kernel(zonal_kernel(r), map, p, p.tiles, s);
+  }
+  if (recon_t == ADCT_RECON_F32) return launch_tma_kernel(k_compress<RT, MODE_ZONAL, REC_F32>, map, p, p.tiles, s);
+  return launch_tma_kernel(k_compress<RT, MODE_ZONAL, REC_U8>, map, p, p.tiles, s);
+}
+
+adct_status adct_psnr(const double* sse, int64_t count, int64_t pixels, double* psnr, adct_stream_t stream) {
+  if (!sse || !psnr || count < 1 || pixels < 1) return ADCT_EINVAL;
+  if (((uintptr_t)sse & 7u) || ((uintptr_t)psnr & 7u)) return ADCT_EALIGN;
+  const int64_t blocks = (count + 255) / 256;
+  k_psnr<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(sse, count, (double)pixels, psnr);
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
+}
+
+adct_status adct_compress_psnr_host(const uint8_t* host_src, int64_t n, int64_t h, int64_t w,
+                                    int64_t host_pitch, int64_t host_img_stride, const int* r_list, int n_r,
+                                    float q, uint8_t* dev_buf, int64_t dev_buf_bytes, double* dev_sse,
+                                    double* host_psnr, adct_stream_t stream) {
+  adct_status st = check_geom(n, h, w);
+  if (st) return st;
+  if (!host_src || !r_list || n_r < 1 || !dev_buf || !dev_sse || !host_psnr) return ADCT_EINVAL;
+  if (host_pitch < w || host_img_stride < h * host_pitch) return ADCT_EINVAL;
+  for (int k = 0; k < n_r; ++k)
+    if (r_list[k] < 1 || r_list[k] > 64) return ADCT_EINVAL;
+  if (!(q >= 0.f) || isinf(q)) return ADCT_EINVAL;
+  const int64_t dpitch = (w + 15) & ~(int64_t)15;
+  const int64_t dimg = dpitch * h;
+  if (!aligned16(dev_buf) || ((uintptr_t)dev_sse & 7u)) return ADCT_EALIGN;
+  const int64_t chunk = dev_buf_bytes / dimg;
+  if (chunk < 1) return ADCT_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int64_t i0 = 0; i0 < n; i0 += chunk) {
+    const int64_t m = (n - i0 < chunk) ? n - i0 : chunk;
+    cudaError_t e;
+    if (host_img_stride == h * host_pitch && host_pitch == dpitch) {
+      e = cudaMemcpyAsync(dev_buf, host_src + i0 * host_img_stride, (size_t)(m * dimg), cudaMemcpyHostToDevice, s);
+    } else {
+      e = cudaSuccess;
+      for (int64_t j = 0; j < m && e == cudaSuccess; ++j)
+        e = cudaMemcpy2DAsync(dev_buf + j * dimg, (size_t)dpitch, host_src + (i0 + j) * host_img_stride,
+                              (size_t)host_pitch, (size_t)w, (size_t)h, cudaMemcpyHostToDevice, s);
+    }
+    if (e != cudaSuccess) return cuda_fail(e);
+    for (int k = 0; k < n_r; ++k) {
+      st = adct_compress_psnr(dev_buf, m, h, w, dpitch, dimg, r_list[k], q, nullptr, ADCT_RECON_NONE, 0, 0,
+                              dev_sse + (int64_t)k * n + i0, stream);
+      if (st) return st;
+    }
+  }
+  // PSNR of every (r, image) into the second half of dev_sse, then one device->host copy
+  double* dev_psnr = dev_sse + (int64_t)n_r * n;
+  if ((st = adct_psnr(dev_sse, n * n_r, h * w, dev_psnr, stream))) return st;
+  cudaError_t e = cudaMemcpyAsync(host_psnr, dev_psnr, sizeof(double) * (size_t)(n * n_r), cudaMemcpyDeviceToHost, s);
+  if (e != cudaSuccess) return cuda_fail(e);
+  return ADCT_OK;
+}
+
+}  // extern "C"
+
+namespace adct {
+CompressKernel zonal_kernel_part0(int r);
+CompressKernel zonal_kernel_part1(int r);
+CompressKernel zonal_kernel_part2(int r);
+CompressKernel zonal_kernel_part3(int r);
+CompressKernel zonal_kernel(int r) {
+  switch ((r - 1) / 16) {
+    case 0: return zonal_kernel_part0(r);
+    case 1: return zonal_kernel_part1(r);
+    case 2: return zonal_kernel_part2(r);
+    default: return zonal_kernel_part3(r);
+  }
+}
+}  // namespace adct

@@ -1,0 +1,390 @@
+// adct_kernels.cuh — sm_100a kernel templates behind the C ABI (include/adct.h) for the arXiv 1402.6034
+// hot path: blockwise 8x8 T X T^T with the 22-addition butterfly, S folded into the zonal /
+// quantisation step, inverse with C^T, per-image SSE -> PSNR.  See DESIGN.md §5 for the
+// data layout and the roofline of each kernel.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "adct_device.cuh"
+
+#include <cuda/std/array>
+
+namespace adct {
+
+enum { MODE_ZONAL = 0, MODE_QUANT = 1 };
+enum { OUT_I16 = 0, OUT_I32 = 1, OUT_F32 = 2 };
+enum { REC_NONE = 0, REC_F32 = 1, REC_U8 = 2 };
+
+struct Tables {
+  float2 w[64];  // ZONAL: (W, W); QUANT: q / sqrt(d_k d_l); INVERSE: per-coef scale — 0 where masked
+  float2 c[64];  // ZONAL: (-KF W, -KF W) [masked: 0]; QUANT: (c', c') quantiser reciprocal
+};
+
+struct CompressParams {
+  TileGeo geo;
+  int64_t tiles;
+  int h, w;
+  double* sse;
+  uint8_t* recon;
+  int64_t recon_pitch, recon_img_stride;
+  Tables tab;
+};
+
+struct ForwardParams {
+  TileGeo geo;
+  int64_t tiles;
+  int h, w;
+  uint8_t* coef;
+  int64_t coef_pitch, coef_img_stride;
+  int masked;        // r < 64
+  uint32_t m16[32];  // I16: AND-mask per coefficient pair (row k, pair m) -> index k*4+m
+  uint64_t keep;     // bit zz: kept
+  float sc[64];      // F32: fp32(1/sqrt(d_i d_j)), 0 where masked
+};
+
+struct InverseParams {
+  TileGeo geo;
+  int64_t tiles;
+  int h, w;
+  const uint8_t* coef;
+  int64_t coef_pitch, coef_img_stride;
+  uint8_t* dst;
+  int64_t dst_pitch, dst_img_stride;
+  Tables tab;  // w[k]: multiplier applied to the loaded coefficient (W or 1/sqrt(dd)), 0 if masked
+};
+
+// ------------------------------------------------------------------------------------------
+// Reconstruction store for row I (8 pixels of block A and of block B) — masked to the image.
+// ------------------------------------------------------------------------------------------
+template <int RECON, bool S576>
+__device__ __forceinline__ void store_recon_row(uint8_t* base, int64_t pitch, int h, int w, int row_a,
+                                                int col, const float2 (&x)[8]) {
+  // S576: x[n] = (R_A[n], R_B[n]) with R = 576 x^ exactly (integers in fp32); else x[n] = x^ itself
+  if (col >= w) return;
+  const int rows[2] = {row_a, row_a + 8};
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    if (rows[b] >= h) continue;
+    uint8_t* p = base + (int64_t)rows[b] * pitch;
+    if constexpr (RECON == REC_F32) {
+      float v[8];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) v[n] = S576 ? (b ? x[n].y : x[n].x) * (1.0f / 576.0f) : (b ? x[n].y : x[n].x);
+      float4* q = reinterpret_cast<float4*>(p + (int64_t)col * 4);
+      q[0] = make_float4(v[0], v[1], v[2], v[3]);
+      q[1] = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+      uint32_t u[8];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        // round_half_away(R / 576) then clamp: floor((R + 288.5) / 576) is exact for integer R
+        const float xv = b ? x[n].y : x[n].x;
+        float t = S576 ? floorf((xv + 288.5f) * (1.0f / 576.0f)) : floorf(xv + 0.5f);
+        t = fminf(fmaxf(t, 0.f), 255.f);
+        u[n] = (uint32_t)t;
+      }
+      uint2 o;
+      o.x = u[0] | (u[1] << 8) | (u[2] << 16) | (u[3] << 24);
+      o.y = u[4] | (u[5] << 8) | (u[6] << 16) | (u[7] << 24);
+      *reinterpret_cast<uint2*>(p + col) = o;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// One warp tile (16 rows x 256 columns) of the fused compress path; returns this lane's
+// partial sum of (576 x - 576 x^)^2 for its two blocks (fp32 pair).
+// ------------------------------------------------------------------------------------------
+template <int R, int MODE, int RECON>
+__device__ __forceinline__ float2 tile_compress(const uint8_t* tile, int lane, const CompressParams& p,
+                                                int img, int ty, int tx) {
+  constexpr int RF = (MODE == MODE_QUANT) ? RT : R;  // forward pruning level
+  uint32_t P[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    pack_rows(lds64(tile + i * TILE_W + lane * 8), lds64(tile + (i + 8) * TILE_W + lane * 8), P[i]);
+  uint32_t Y[8][8];
+  fwd2d<BIAS2, RF>(P, Y);
+
+  float2 V[64];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+      if (!kept(RF, k, l)) continue;
+      const int kl = k * 8 + l;
+      if constexpr (MODE == MODE_ZONAL) {
+        V[kl] = f2fma(biased_pair(Y[k][l]), p.tab.w[kl], p.tab.c[kl]);  // W . M . Y, exact
+      } else {
+        const float2 y = f2add(biased_pair(Y[k][l]), f2(-KF));          // Y, exact
+        // 1.5*2^23 + RN(Y c'): c' lies strictly above 1/(q sqrt dd), so exact ties of Z/q round
+        // away from zero and no product Y c' is itself a tie (reading R10)
+        const float2 t = f2fma(y, p.tab.c[kl], f2(12582912.0f));
+        V[kl] = __fmul2_rn(f2add(t, f2(-12582912.0f)), p.tab.w[kl]);     // q k / sqrt(dd) (M folded)
+      }
+    }
+  }
+
+  float2 acc = f2(0.f);
+  const int col = tx * TILE_W + lane * 8;
+  uint8_t* rbase = nullptr;
+  if constexpr (RECON != REC_NONE) rbase = p.recon + (int64_t)img * p.recon_img_stride;
+  inverse2d<RF>(V, [&](auto Ic, auto row) {
+    constexpr int I = decltype(Ic)::value;
+    using cuda::std::get;
+    const uint2 wa = lds64(tile + I * TILE_W + lane * 8);
+    const uint2 wb = lds64(tile + (I + 8) * TILE_W + lane * 8);
+    float2 xr[8];
+    static_for<8>([&](auto Nc) {
+      constexpr int N = decltype(Nc)::value;
+      // ZONAL: 576 x - R, exact integers; QUANT: x - x^ (fp32, irrational weights)
+      const float2 y = (MODE == MODE_ZONAL) ? px576(N < 4 ? wa.x : wa.y, N < 4 ? wb.x : wb.y, N & 3)
+                                            : px1(N < 4 ? wa.x : wa.y, N < 4 ? wb.x : wb.y, N & 3);
+      const float2 e = rsub(y, get<N>(row));
+      acc = f2fma(e, e, acc);
+      if constexpr (RECON != REC_NONE) xr[N] = val(get<N>(row));
+    });
+    if constexpr (RECON != REC_NONE)
+      store_recon_row<RECON, (MODE == MODE_ZONAL)>(rbase, p.recon_pitch, p.h, p.w, ty * TILE_H + I, col, xr);
+  });
+  return acc;
+}
+
+template <int R, int MODE, int RECON>
+__global__ void __launch_bounds__(WARPS * 32, 3)
+    k_compress(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CompressParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr double kSseScale = (MODE == MODE_ZONAL) ? 1.0 / 331776.0 : 1.0;  // errors in 576 units (ZONAL)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = smem + warp * (STAGES * TILE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * STAGES * TILE_BYTES) + warp * STAGES;
+
+  const int64_t G = (int64_t)gridDim.x * WARPS;
+  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
+  const int64_t t0 = gw * p.tiles / G, t1 = (gw + 1) * p.tiles / G;
+  if (t0 >= t1) return;
+
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    fence_mbar_init();
+    for (int s = 0; s < STAGES && t0 + s < t1; ++s) {
+      int img, ty, tx;
+      p.geo.decode(t0 + s, img, ty, tx);
+      mbar_expect_tx(smem_u32(&bars[s]), TILE_BYTES);
+      tma_load_3d(smem_u32(ring + s * TILE_BYTES), &tmap, tx * TILE_W, ty * TILE_H, img,
+                  smem_u32(&bars[s]));
+    }
+  }
+  __syncwarp();
+
+  int cur = -1;
+  double acc = 0.0;
+  int s = 0;
+  uint32_t parity = 0;
+  for (int64_t t = t0; t < t1; ++t) {
+    int img, ty, tx;
+    p.geo.decode(t, img, ty, tx);
+    if (img != cur) {  // warp-uniform: flush the finished image's partial SSE
+      const double v = warp_sum(acc);
+      if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v * kSseScale);
+      cur = img;
+      acc = 0.0;
+    }
+    mbar_wait(smem_u32(&bars[s]), parity);
+    const float2 e2 = tile_compress<R, MODE, RECON>(ring + s * TILE_BYTES, lane, p, img, ty, tx);
+    acc += (double)e2.x + (double)e2.y;
+    __syncwarp();
+    if (lane == 0 && t + STAGES < t1) {
+      int img2, ty2, tx2;
+      p.geo.decode(t + STAGES, img2, ty2, tx2);
+      fence_proxy_async();  // generic-proxy reads of this stage precede the async-proxy refill
+      mbar_expect_tx(smem_u32(&bars[s]), TILE_BYTES);
+      tma_load_3d(smem_u32(ring + s * TILE_BYTES), &tmap, tx2 * TILE_W, ty2 * TILE_H, img2,
+                  smem_u32(&bars[s]));
+    }
+    if (++s == STAGES) {
+      s = 0;
+      parity ^= 1u;
+    }
+  }
+  const double v = warp_sum(acc);
+  if (lane == 0) atomicAdd(p.sse + cur, v * kSseScale);
+}
+
+// ------------------------------------------------------------------------------------------
+// Forward only: Y (int16 / int32) or Z (fp32) image-shaped.
+// ------------------------------------------------------------------------------------------
+template <int OUT>
+__device__ __forceinline__ void tile_forward(const uint8_t* tile, int lane, const ForwardParams& p, int img,
+                                             int ty, int tx) {
+  constexpr uint32_t K = (OUT == OUT_F32) ? BIAS2 : 0x8000u;
+  uint32_t P[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    pack_rows(lds64(tile + i * TILE_W + lane * 8), lds64(tile + (i + 8) * TILE_W + lane * 8), P[i]);
+  uint32_t Y[8][8];
+  fwd2d<K, 64>(P, Y);
+  const int col = tx * TILE_W + lane * 8;
+  if (col >= p.w) return;
+  uint8_t* base = p.coef + (int64_t)img * p.coef_img_stride;
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int row = ty * TILE_H + b * 8 + k;
+      if (row >= p.h) continue;
+      uint8_t* rp = base + (int64_t)row * p.coef_pitch;
+      if constexpr (OUT == OUT_I16) {
+        uint32_t o[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          o[m] = b ? __byte_perm(Y[k][2 * m], Y[k][2 * m + 1], 0x7632)
+                   : (__byte_perm(Y[k][2 * m], Y[k][2 * m + 1], 0x5410) ^ 0x80008000u);
+          if (p.masked) o[m] &= p.m16[k * 4 + m];
+        }
+        *reinterpret_cast<uint4*>(rp + (int64_t)col * 2) = make_uint4(o[0], o[1], o[2], o[3]);
+      } else if constexpr (OUT == OUT_I32) {
+        int v[8];
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+          v[l] = b ? ((int32_t)Y[k][l] >> 16) : ((int)(Y[k][l] & 0xFFFFu) - 32768);
+          if (p.masked && !((p.keep >> zz_index(k, l)) & 1ull)) v[l] = 0;
+        }
+        int4* q = reinterpret_cast<int4*>(rp + (int64_t)col * 4);
+        q[0] = make_int4(v[0], v[1], v[2], v[3]);
+        q[1] = make_int4(v[4], v[5], v[6], v[7]);
+      } else {
+        float v[8];
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+          const float2 y = f2add(biased_pair(Y[k][l]), f2(-KF));
+          v[l] = (b ? y.y : y.x) * p.sc[k * 8 + l];
+        }
+        float4* q = reinterpret_cast<float4*>(rp + (int64_t)col * 4);
+        q[0] = make_float4(v[0], v[1], v[2], v[3]);
+        q[1] = make_float4(v[4], v[5], v[6], v[7]);
+      }
+    }
+  }
+}
+
+template <int OUT>
+__global__ void __launch_bounds__(WARPS * 32, 3)
+    k_forward(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ForwardParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = smem + warp * (STAGES * TILE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * STAGES * TILE_BYTES) + warp * STAGES;
+  const int64_t G = (int64_t)gridDim.x * WARPS;
+  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
+  const int64_t t0 = gw * p.tiles / G, t1 = (gw + 1) * p.tiles / G;
+  if (t0 >= t1) return;
+  if (lane == 0) {
+#pragma unroll
+    for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&bars[s]), 1);
+    fence_mbar_init();
+    for (int s = 0; s < STAGES && t0 + s < t1; ++s) {
+      int img, ty, tx;
+      p.geo.decode(t0 + s, img, ty, tx);
+      mbar_expect_tx(smem_u32(&bars[s]), TILE_BYTES);
+      tma_load_3d(smem_u32(ring + s * TILE_BYTES), &tmap, tx * TILE_W, ty * TILE_H, img,
+                  smem_u32(&bars[s]));
+    }
+  }
+  __syncwarp();
+  int s = 0;
+  uint32_t parity = 0;
+  for (int64_t t = t0; t < t1; ++t) {
+    int img, ty, tx;
+    p.geo.decode(t, img, ty, tx);
+    mbar_wait(smem_u32(&bars[s]), parity);
+    tile_forward<OUT>(ring + s * TILE_BYTES, lane, p, img, ty, tx);
+    __syncwarp();
+    if (lane == 0 && t + STAGES < t1) {
+      int img2, ty2, tx2;
+      p.geo.decode(t + STAGES, img2, ty2, tx2);
+      fence_proxy_async();
+      mbar_expect_tx(smem_u32(&bars[s]), TILE_BYTES);
+      tma_load_3d(smem_u32(ring + s * TILE_BYTES), &tmap, tx2 * TILE_W, ty2 * TILE_H, img2,
+                  smem_u32(&bars[s]));
+    }
+    if (++s == STAGES) {
+      s = 0;
+      parity ^= 1u;
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// Inverse only: coefficient plane -> reconstruction (direct vectorised loads; no staging).
+// ------------------------------------------------------------------------------------------
+template <int IN>
+__device__ __forceinline__ void load_coef_row(const uint8_t* rp, bool ok, float (&v)[8]) {
+  if (!ok) {
+#pragma unroll
+    for (int l = 0; l < 8; ++l) v[l] = 0.f;
+    return;
+  }
+  if constexpr (IN == OUT_I16) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(rp));
+    const uint32_t w4[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      v[2 * m] = (float)(int16_t)(w4[m] & 0xFFFFu);
+      v[2 * m + 1] = (float)(int16_t)(w4[m] >> 16);
+    }
+  } else if constexpr (IN == OUT_I32) {
+    const int4 a = __ldg(reinterpret_cast<const int4*>(rp)), b = __ldg(reinterpret_cast<const int4*>(rp) + 1);
+    v[0] = (float)a.x; v[1] = (float)a.y; v[2] = (float)a.z; v[3] = (float)a.w;
+    v[4] = (float)b.x; v[5] = (float)b.y; v[6] = (float)b.z; v[7] = (float)b.w;
+  } else {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(rp)), b = __ldg(reinterpret_cast<const float4*>(rp) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+}
+
+template <int IN, int RECON>
+__global__ void __launch_bounds__(WARPS * 32, 3) k_inverse(const __grid_constant__ InverseParams p) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int ES = (IN == OUT_I16) ? 2 : 4;
+  for (int64_t t = (int64_t)blockIdx.x * WARPS + warp; t < p.tiles; t += (int64_t)gridDim.x * WARPS) {
+    int img, ty, tx;
+    p.geo.decode(t, img, ty, tx);
+    const int col = tx * TILE_W + lane * 8;
+    const bool cok = col < p.w;
+    const uint8_t* base = p.coef + (int64_t)img * p.coef_img_stride + (int64_t)col * ES;
+    float2 V[64];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float a[8], b[8];
+      const int ra = ty * TILE_H + k, rb = ra + 8;
+      load_coef_row<IN>(base + (int64_t)ra * p.coef_pitch, cok && ra < p.h, a);
+      load_coef_row<IN>(base + (int64_t)rb * p.coef_pitch, cok && rb < p.h, b);
+#pragma unroll
+      for (int l = 0; l < 8; ++l) V[k * 8 + l] = __fmul2_rn(make_float2(a[l], b[l]), p.tab.w[k * 8 + l]);
+    }
+    uint8_t* dbase = p.dst + (int64_t)img * p.dst_img_stride;
+    inverse2d<RT>(V, [&](auto Ic, auto row) {
+      constexpr int I = decltype(Ic)::value;
+      float2 xr[8];
+      static_for<8>([&](auto Nc) {
+        constexpr int N = decltype(Nc)::value;
+        xr[N] = val(cuda::std::get<N>(row));
+      });
+      store_recon_row<RECON, true>(dbase, p.dst_pitch, p.h, p.w, ty * TILE_H + I, col, xr);
+    });
+  }
+}
+
+typedef void (*CompressKernel)(CUtensorMap, CompressParams);
+// zonal kernels k_compress<r, ZONAL, RECON_NONE>, instantiated in zonal_part*.cu (4 TUs)
+CompressKernel zonal_kernel(int r);
+
+}  // namespace adct
+

@@ -1,0 +1,314 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle on the same seeded
+inputs.  Bars (BASELINE.json north_star): integer coefficients bit-exact; fp32 coefficients and
+reconstructions max |err| <= 1e-4 on the 0-255 scale; PSNR within 1e-3 dB.
+
+SSE tolerance: each lane sums its 128 exact squared errors (576 x - 576 x^)^2
+with fused fp32 FMAs, so the relative error of a lane's partial is at most 127 u = 7.6e-6
+(u = 2^-24); partials are then combined in fp64.  SSE_RTOL = 1e-5 bounds that, and maps to
+|dPSNR| <= 4.4e-5 dB, inside the 1e-3 dB bar.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+from synth import images as S
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a CUDA device")]
+
+import paper_1402_6034_b200 as A  # noqa: E402
+
+FP_TOL = 1e-4
+SSE_RTOL = 1e-5
+PSNR_TOL = 1e-3
+rng = np.random.default_rng(99)
+
+
+def dev(x):
+    """16-byte-pitched device copy (the ABI requires pitch % 16 == 0)."""
+    return A.to_device(x)
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def check_sse(got, want, pixels):
+    """SSE within SSE_RTOL (floor: MSE 1e-6) and PSNR within PSNR_TOL where the MSE is >= 1e-6.
+
+    Below MSE 1e-6 (PSNR > 108 dB) both sides are lossless up to the oracle's own float64
+    round-off (it reports ~1e-25 where the exact SSE is 0), so only the SSE bound applies.
+    """
+    got, want = np.asarray(got, float), np.asarray(want, float)
+    floor = 1e-6 * pixels
+    assert np.all(np.abs(got - want) <= SSE_RTOL * np.maximum(np.abs(want), floor)), (got, want)
+    big = want >= floor
+    assert np.all(np.abs(O.psnr(got[big], pixels) - O.psnr(want[big], pixels)) <= PSNR_TOL)
+
+
+def impulse_images():
+    """128 single-block images: value 1 and value 255 at each of the 64 positions."""
+    imgs = np.zeros((128, 8, 8), dtype=np.uint8)
+    for p in range(64):
+        imgs[p, p // 8, p % 8] = 1
+        imgs[64 + p, p // 8, p % 8] = 255
+    return imgs
+
+
+def extreme_images():
+    imgs = [np.zeros((8, 8)), np.full((8, 8), 255)]
+    ii, jj = np.indices((8, 8))
+    imgs += [255 * ((ii + jj) % 2), 255 * ((ii + jj + 1) % 2), 255 * (ii % 2), 255 * (jj % 2)]
+    imgs += [rng.choice([0, 255], size=(8, 8)) for _ in range(58)]
+    return np.stack(imgs).astype(np.uint8)
+
+
+# ------------------------------------------------------------------ forward (integer, exact)
+
+@pytest.mark.parametrize("coef", ["i16", "i32"])
+def test_forward_integer_bit_exact_blocks(coef):
+    for imgs in (impulse_images(), extreme_images(), rng.integers(0, 256, (300, 8, 8), dtype=np.uint8)):
+        Y = host(A.forward(dev(imgs), coef=coef))
+        assert np.array_equal(Y.astype(np.int64), O.forward_int(imgs))
+
+
+@pytest.mark.parametrize("h,w", [(8, 8), (16, 16), (8, 504), (24, 520), (512, 512), (40, 264), (264, 8)])
+def test_forward_shapes_and_ragged_tiles(h, w):
+    imgs = rng.integers(0, 256, (3, h, w), dtype=np.uint8)
+    Y = host(A.forward(dev(imgs)))
+    assert np.array_equal(Y.astype(np.int64), O.forward_int(imgs))
+
+
+def test_forward_c1_and_c3_subset_bit_exact():
+    c1 = S.image_c1(0)
+    assert np.array_equal(host(A.forward(dev(c1)))[0].astype(np.int64), O.forward_int(c1)[0])
+    x = S.device_uniform(64, 512, 512, seed=0)       # C3 recipe, 64-image subset
+    Y = host(A.forward(x)).astype(np.int64)
+    assert np.array_equal(Y, O.forward_int(host(x)))
+
+
+def test_forward_pitch_and_image_stride():
+    base = torch.zeros((3, 40, 96), dtype=torch.uint8, device="cuda")
+    imgs = rng.integers(0, 256, (3, 32, 64), dtype=np.uint8)
+    base[:, :32, :64] = dev(imgs)
+    view = base[:, :32, :64]                                   # pitch 96, image stride 40*96
+    out = torch.full((3, 48, 80), 7, dtype=torch.int16, device="cuda")
+    A.forward(view, out=out[:, :32, :64])
+    got = host(out)
+    assert np.array_equal(got[:, :32, :64].astype(np.int64), O.forward_int(imgs))
+    assert np.all(got[:, 32:, :] == 7) and np.all(got[:, :, 64:] == 7)   # nothing written outside
+
+
+@pytest.mark.parametrize("r", [1, 3, 5, 10, 21, 36, 50, 63])
+def test_forward_masked(r):
+    imgs = rng.integers(0, 256, (4, 32, 48), dtype=np.uint8)
+    want = O.from_blocks(O.to_blocks(O.forward_int(imgs)) * O.zonal_mask(r))
+    for coef in ("i16", "i32"):
+        assert np.array_equal(host(A.forward(dev(imgs), r=r, coef=coef)).astype(np.int64), want)
+    Z = host(A.forward(dev(imgs), r=r, coef="f32"))
+    Zw = O.from_blocks(O.to_blocks(O.forward_scaled(imgs)) * O.zonal_mask(r))
+    assert np.abs(Z - Zw).max() <= FP_TOL
+
+
+def test_forward_scaled_f32():
+    imgs = np.concatenate([extreme_images(), rng.integers(0, 256, (200, 8, 8), dtype=np.uint8)])
+    Z = host(A.forward(dev(imgs), coef="f32"))
+    assert np.abs(Z - O.forward_scaled(imgs)).max() <= FP_TOL
+
+
+# ------------------------------------------------------------------ inverse
+
+@pytest.mark.parametrize("r", [1, 4, 10, 28, 64])
+def test_inverse_from_integer_and_scaled(r):
+    imgs = np.concatenate([S.corpus_c2(3, 64, 64).reshape(-1, 64, 64)])
+    want = O.reconstruct_zonal(imgs, r)
+    Y = O.forward_int(imgs).astype(np.int16)
+    rec = host(A.inverse(dev(Y), r=r, out="f32"))
+    assert np.abs(rec - want).max() <= FP_TOL
+    rec32 = host(A.inverse(dev(Y.astype(np.int32)), r=r))
+    assert np.abs(rec32 - want).max() <= FP_TOL
+    Z = O.forward_scaled(imgs).astype(np.float32)
+    recz = host(A.inverse(dev(Z), r=r))
+    assert np.abs(recz - want).max() <= FP_TOL
+    u8 = host(A.inverse(dev(Y), r=r, out="u8"))
+    R = O.reconstruct_zonal_exact(imgs, r)
+    assert np.array_equal(u8, O.round_u8(R / 576.0))
+
+
+# ------------------------------------------------------------------ fused compress (zonal)
+
+def test_compress_c1_r10():
+    """BASELINE C1: one 512x512 image, r = 10, PSNR."""
+    img = S.image_c1(0)
+    sse = host(A.compress_psnr(dev(img), 10))
+    check_sse(sse, O.compress_zonal_sse(img, 10), 512 * 512)
+
+
+def test_compress_every_r_c2_like():
+    imgs = S.corpus_c2(6, 128, 128)
+    x = dev(imgs)
+    for r in range(1, 65):
+        sse = host(A.compress_psnr(x, r))
+        want = O.compress_zonal_sse(imgs, r)
+        if r == 64:
+            assert np.all(sse < 1e-6)
+            assert np.all(np.isinf(host(A.psnr(A.compress_psnr(x, r), 128 * 128))))
+        else:
+            check_sse(sse, want, 128 * 128)
+
+
+def test_compress_c2_full_mean_psnr():
+    """BASELINE C2 (45 x 512^2): mean PSNR per r for the proposed transform vs the oracle."""
+    imgs = S.corpus_c2()
+    x = dev(imgs)
+    for r in (1, 2, 5, 10, 16, 45):
+        sse = host(A.compress_psnr(x, r))
+        want = O.compress_zonal_sse(imgs, r)
+        check_sse(sse, want, 512 * 512)
+        assert abs(O.mean_psnr(sse, 512 * 512) - O.mean_psnr(want, 512 * 512)) <= PSNR_TOL
+
+
+@pytest.mark.parametrize("r", [1, 3, 6, 10, 15, 21, 28, 36, 7, 50])
+def test_compress_recon_f32_and_u8(r):
+    imgs = np.concatenate([S.corpus_c2(3, 64, 96),
+                           rng.choice(np.array([0, 255], dtype=np.uint8), size=(2, 64, 96))])
+    want = O.reconstruct_zonal(imgs, r)
+    sse, rec = A.compress_psnr(dev(imgs), r, recon="f32")
+    assert np.abs(host(rec) - want).max() <= FP_TOL
+    check_sse(host(sse), O.compress_zonal_sse(imgs, r), 64 * 96)
+    sse2, rec8 = A.compress_psnr(dev(imgs), r, recon="u8")
+    R = O.reconstruct_zonal_exact(imgs, r)
+    assert np.array_equal(host(rec8), O.round_u8(R / 576.0))
+    assert np.allclose(host(sse2), host(sse), rtol=1e-12)
+
+
+@pytest.mark.parametrize("h,w", [(8, 8), (8, 16), (24, 504), (40, 264), (264, 8), (16, 520)])
+def test_compress_ragged_shapes(h, w):
+    imgs = rng.integers(0, 256, (5, h, w), dtype=np.uint8)
+    for r in (1, 10, 36, 64):
+        sse = host(A.compress_psnr(dev(imgs), r))
+        want = O.compress_zonal_sse(imgs, r)
+        if r == 64:
+            assert np.all(sse < 1e-6)
+        else:
+            check_sse(sse, want, h * w)
+
+
+def test_compress_extremes_and_impulses():
+    for imgs in (impulse_images(), extreme_images()):
+        for r in (1, 2, 9, 33, 63):
+            check_sse(host(A.compress_psnr(dev(imgs), r)), O.compress_zonal_sse(imgs, r), 64)
+
+
+def test_compress_c5_pattern_blocks_closed_form():
+    """Full C5 image size (4096^2): tiled pattern blocks have an analytic SSE at every r (P17)."""
+    T = O.c0_matrix()
+    d = np.array([8, 6, 4, 6, 8, 6, 4, 6])
+    zz = O.zigzag_index()
+    img, I, J, Am = S.pattern_image_from_rows(T, 4096, 4096, seed=3)
+    x = dev(img[None])
+    for r in (1, 3, 6, 10, 15, 21, 28, 36):
+        want = float(np.sum(np.where(zz[I, J] < r, 0, Am.astype(np.int64) ** 2 * d[I] * d[J])))
+        sse = host(A.compress_psnr(x, r))[0]
+        assert abs(sse - want) <= SSE_RTOL * want, (r, sse, want)
+
+
+def test_compress_c5_sampled_images_vs_oracle():
+    """Three C5 images (one per kind) generated on the device, all 8 C5 r values."""
+    x = S.device_mixed(3, 4096, 4096, seed=0)
+    imgs = host(x)
+    for r in (1, 10, 36):
+        check_sse(host(A.compress_psnr(x, r)), O.compress_zonal_sse(imgs, r), 4096 * 4096)
+
+
+# ------------------------------------------------------------------ fused compress (quantiser)
+
+@pytest.mark.parametrize("q", [16.0, 5.0, 3.0])
+def test_compress_quant_vs_oracle(q):
+    imgs = np.concatenate([S.corpus_c2(3, 64, 64), rng.integers(0, 256, (2, 64, 64), dtype=np.uint8)])
+    want = O.reconstruct_quant(imgs, q)
+    sse, rec = A.compress_psnr(dev(imgs), 64, q=q, recon="f32")
+    assert np.abs(host(rec) - want).max() <= FP_TOL
+    check_sse(host(sse), O.sse_per_image(imgs, want), 64 * 64)
+    sse_only = host(A.compress_psnr(dev(imgs), 64, q=q))
+    assert np.allclose(sse_only, host(sse), rtol=1e-12)
+
+
+def test_compress_quant_c4_constant_frames_closed_form():
+    """Full C4 frame size 4320 x 7680: constant frames under q = 16 (P18): odd v -> MSE 1."""
+    vals = [0, 1, 128, 255]
+    x = torch.stack([torch.full((4320, 7680), v, dtype=torch.uint8, device="cuda") for v in vals])
+    sse = host(A.compress_psnr(x, 64, q=16.0))
+    for v, s in zip(vals, sse):
+        assert s == (4320 * 7680 if v % 2 else 0.0)
+
+
+def test_compress_quant_c4_frame_vs_oracle():
+    x = S.device_video(2, 4320, 7680, seed=0)
+    imgs = host(x)
+    sse = host(A.compress_psnr(x, 64, q=16.0))
+    check_sse(sse, O.compress_quant_sse(imgs, 16.0), 4320 * 7680)
+
+
+# ------------------------------------------------------------------ ABI behaviour on the device
+
+def test_errors_enqueue_nothing():
+    x = torch.zeros((2, 16, 16), dtype=torch.uint8, device="cuda")
+    sse = torch.full((2,), 123.0, dtype=torch.float64, device="cuda")
+    for kw in (dict(r=0), dict(r=65), dict(q=-1.0)):
+        with pytest.raises(A.AdctError):
+            A.compress_psnr(x, kw.get("r", 10), q=kw.get("q", 0.0), sse=sse)
+    with pytest.raises(A.AdctError):
+        A.compress_psnr(torch.zeros((2, 12, 16), dtype=torch.uint8, device="cuda"), 10, sse=sse)
+    buf = torch.zeros((2 * 16 * 16 + 1,), dtype=torch.uint8, device="cuda")
+    with pytest.raises(A.AdctError) as e:
+        A.compress_psnr(buf[1:].view(2, 16, 16), 10, sse=sse)
+    assert e.value.status == 2
+    assert np.all(host(sse) == 123.0)
+
+
+def test_streams_and_determinism():
+    imgs = S.corpus_c2(4, 256, 256)
+    x = dev(imgs)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s1):
+        a = A.compress_psnr(x, 10)
+    with torch.cuda.stream(s2):
+        b = A.compress_psnr(x, 10)
+    torch.cuda.synchronize()
+    assert np.allclose(host(a), host(b), rtol=1e-13)
+    c = host(A.compress_psnr(x, 10))
+    assert np.allclose(c, host(a), rtol=1e-13)
+
+
+def test_end_to_end_host_entry_matches_device_path():
+    imgs = S.corpus_c2(6, 128, 128)
+    rs = [1, 3, 6, 10, 15, 21, 28, 36]
+    pinned = torch.from_numpy(imgs).pin_memory()
+    dev_buf = torch.empty((2 * 128 * 128,), dtype=torch.uint8, device="cuda")   # forces chunking
+    ps = A.compress_psnr_host(pinned, rs, dev_buf=dev_buf)
+    torch.cuda.synchronize()
+    for k, r in enumerate(rs):
+        want = O.psnr(O.compress_zonal_sse(imgs, r), 128 * 128)
+        assert np.all(np.abs(ps[k].numpy() - want) <= PSNR_TOL)
+
+
+def test_launch_count_increments():
+    x = torch.zeros((1, 16, 16), dtype=torch.uint8, device="cuda")
+    n0 = A.launch_count()
+    A.compress_psnr(x, 3)
+    A.forward(x)
+    torch.cuda.synchronize()
+    assert A.launch_count() == n0 + 2
+
+
+def test_psnr_kernel():
+    sse = torch.tensor([0.0, 64.0, 256.0 * 4], dtype=torch.float64, device="cuda")
+    p = host(A.psnr(sse, 64))
+    assert np.isinf(p[0]) and abs(p[1] - 20 * math.log10(255)) < 1e-12
+    assert abs(p[2] - O.psnr(1024.0, 64)) < 1e-12
