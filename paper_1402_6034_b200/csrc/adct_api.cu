@@ -135,8 +135,9 @@ void fill_quant_tables(Tables& t, int r, float q) {
 }
 
 template <class K, class P>
-adct_status launch_tma_kernel(K kern, const CUtensorMap& map, const P& params, int64_t tiles,
+adct_status launch_tma_kernel(K kern, const CUtensorMap& map, const P& params_in, int64_t tiles,
                               cudaStream_t stream) {
+  P params = params_in;
   const int smem = WARPS * STAGES * TILE_BYTES + WARPS * STAGES * 8;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return cuda_fail(e);
@@ -147,7 +148,12 @@ adct_status launch_tma_kernel(K kern, const CUtensorMap& map, const P& params, i
   if (e != cudaSuccess) return cuda_fail(e);
   if (occ < 1) occ = 1;
   int64_t grid = (int64_t)sms * occ;
-  const int64_t need = (tiles + WARPS - 1) / WARPS;
+  // chunk = largest power of two <= 16 that still gives every resident warp >= 2 chunks
+  int cshift = 4;
+  while (cshift > 0 && (tiles >> cshift) < 2 * grid * WARPS) --cshift;
+  params.cshift = cshift;
+  const int64_t chunks = (tiles + (int64_t(1) << cshift) - 1) >> cshift;
+  const int64_t need = (chunks + WARPS - 1) / WARPS;
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
   kern<<<(unsigned)grid, WARPS * 32, smem, stream>>>(map, params);
@@ -197,7 +203,10 @@ adct_status adct_forward(const uint8_t* src, int64_t n, int64_t h, int64_t w, in
   p.coef_pitch = coef_pitch;
   p.coef_img_stride = coef_img_stride;
   p.masked = r < 64;
-  p.keep = (r >= 64) ? ~0ull : ((1ull << r) - 1ull);
+  p.keep_raster = 0;
+  for (int k = 0; k < 8; ++k)
+    for (int l = 0; l < 8; ++l)
+      if (zz_host(k, l) < r) p.keep_raster |= 1ull << (k * 8 + l);
   for (int k = 0; k < 8; ++k)
     for (int m = 0; m < 4; ++m) {
       uint32_t mk = 0;

@@ -27,6 +27,7 @@ struct Tables {
 struct CompressParams {
   TileGeo geo;
   int64_t tiles;
+  int cshift;  // log2 tiles per scheduling chunk
   int h, w;
   double* sse;
   uint8_t* recon;
@@ -37,12 +38,13 @@ struct CompressParams {
 struct ForwardParams {
   TileGeo geo;
   int64_t tiles;
+  int cshift;
   int h, w;
   uint8_t* coef;
   int64_t coef_pitch, coef_img_stride;
   int masked;        // r < 64
   uint32_t m16[32];  // I16: AND-mask per coefficient pair (row k, pair m) -> index k*4+m
-  uint64_t keep;     // bit zz: kept
+  uint64_t keep_raster;  // bit k*8+l: coefficient (k, l) kept
   float sc[64];      // F32: fp32(1/sqrt(d_i d_j)), 0 where masked
 };
 
@@ -111,12 +113,9 @@ __device__ __forceinline__ float2 tile_compress(const uint8_t* tile, int lane, c
   fwd2d<BIAS2, RF>(P, Y);
 
   float2 V[64];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-#pragma unroll
-    for (int l = 0; l < 8; ++l) {
-      if (!kept(RF, k, l)) continue;
-      const int kl = k * 8 + l;
+  static_for<64>([&](auto KLc) {
+    constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
+    if constexpr (kept(RF, k, l)) {
       if constexpr (MODE == MODE_ZONAL) {
         V[kl] = f2fma(biased_pair(Y[k][l]), p.tab.w[kl], p.tab.c[kl]);  // W . M . Y, exact
       } else {
@@ -127,7 +126,7 @@ __device__ __forceinline__ float2 tile_compress(const uint8_t* tile, int lane, c
         V[kl] = __fmul2_rn(f2add(t, f2(-12582912.0f)), p.tab.w[kl]);     // q k / sqrt(dd) (M folded)
       }
     }
-  }
+  });
 
   float2 acc = f2(0.f);
   const int col = tx * TILE_W + lane * 8;
@@ -163,57 +162,21 @@ __global__ void __launch_bounds__(WARPS * 32, 3)
   uint8_t* ring = smem + warp * (STAGES * TILE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * STAGES * TILE_BYTES) + warp * STAGES;
 
-  const int64_t G = (int64_t)gridDim.x * WARPS;
-  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
-  const int64_t t0 = gw * p.tiles / G, t1 = (gw + 1) * p.tiles / G;
-  if (t0 >= t1) return;
-
-  if (lane == 0) {
-#pragma unroll
-    for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&bars[s]), 1);
-    fence_mbar_init();
-    for (int s = 0; s < STAGES && t0 + s < t1; ++s) {
-      int img, ty, tx;
-      p.geo.decode(t0 + s, img, ty, tx);
-      mbar_expect_tx(smem_u32(&bars[s]), TILE_BYTES);
-      tma_load_3d(smem_u32(ring + s * TILE_BYTES), &tmap, tx * TILE_W, ty * TILE_H, img,
-                  smem_u32(&bars[s]));
-    }
-  }
-  __syncwarp();
-
+  const WarpSched ws{(int64_t)blockIdx.x * WARPS + warp, (int64_t)gridDim.x * WARPS, p.tiles, p.cshift};
   int cur = -1;
   double acc = 0.0;
-  int s = 0;
-  uint32_t parity = 0;
-  for (int64_t t = t0; t < t1; ++t) {
-    int img, ty, tx;
-    p.geo.decode(t, img, ty, tx);
+  tma_ring_loop(&tmap, ws, p.geo, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {  // warp-uniform: flush the finished image's partial SSE
       const double v = warp_sum(acc);
       if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v * kSseScale);
       cur = img;
       acc = 0.0;
     }
-    mbar_wait(smem_u32(&bars[s]), parity);
-    const float2 e2 = tile_compress<R, MODE, RECON>(ring + s * TILE_BYTES, lane, p, img, ty, tx);
+    const float2 e2 = tile_compress<R, MODE, RECON>(tile, lane, p, img, ty, tx);
     acc += (double)e2.x + (double)e2.y;
-    __syncwarp();
-    if (lane == 0 && t + STAGES < t1) {
-      int img2, ty2, tx2;
-      p.geo.decode(t + STAGES, img2, ty2, tx2);
-      fence_proxy_async();  // generic-proxy reads of this stage precede the async-proxy refill
-      mbar_expect_tx(smem_u32(&bars[s]), TILE_BYTES);
-      tma_load_3d(smem_u32(ring + s * TILE_BYTES), &tmap, tx2 * TILE_W, ty2 * TILE_H, img2,
-                  smem_u32(&bars[s]));
-    }
-    if (++s == STAGES) {
-      s = 0;
-      parity ^= 1u;
-    }
-  }
+  });
   const double v = warp_sum(acc);
-  if (lane == 0) atomicAdd(p.sse + cur, v * kSseScale);
+  if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v * kSseScale);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -253,7 +216,7 @@ __device__ __forceinline__ void tile_forward(const uint8_t* tile, int lane, cons
 #pragma unroll
         for (int l = 0; l < 8; ++l) {
           v[l] = b ? ((int32_t)Y[k][l] >> 16) : ((int)(Y[k][l] & 0xFFFFu) - 32768);
-          if (p.masked && !((p.keep >> zz_index(k, l)) & 1ull)) v[l] = 0;
+          if (p.masked && !((p.keep_raster >> (k * 8 + l)) & 1ull)) v[l] = 0;
         }
         int4* q = reinterpret_cast<int4*>(rp + (int64_t)col * 4);
         q[0] = make_int4(v[0], v[1], v[2], v[3]);
@@ -280,44 +243,10 @@ __global__ void __launch_bounds__(WARPS * 32, 3)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* ring = smem + warp * (STAGES * TILE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * STAGES * TILE_BYTES) + warp * STAGES;
-  const int64_t G = (int64_t)gridDim.x * WARPS;
-  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp;
-  const int64_t t0 = gw * p.tiles / G, t1 = (gw + 1) * p.tiles / G;
-  if (t0 >= t1) return;
-  if (lane == 0) {
-#pragma unroll
-    for (int s = 0; s < STAGES; ++s) mbar_init(smem_u32(&bars[s]), 1);
-    fence_mbar_init();
-    for (int s = 0; s < STAGES && t0 + s < t1; ++s) {
-      int img, ty, tx;
-      p.geo.decode(t0 + s, img, ty, tx);
-      mbar_expect_tx(smem_u32(&bars[s]), TILE_BYTES);
-      tma_load_3d(smem_u32(ring + s * TILE_BYTES), &tmap, tx * TILE_W, ty * TILE_H, img,
-                  smem_u32(&bars[s]));
-    }
-  }
-  __syncwarp();
-  int s = 0;
-  uint32_t parity = 0;
-  for (int64_t t = t0; t < t1; ++t) {
-    int img, ty, tx;
-    p.geo.decode(t, img, ty, tx);
-    mbar_wait(smem_u32(&bars[s]), parity);
-    tile_forward<OUT>(ring + s * TILE_BYTES, lane, p, img, ty, tx);
-    __syncwarp();
-    if (lane == 0 && t + STAGES < t1) {
-      int img2, ty2, tx2;
-      p.geo.decode(t + STAGES, img2, ty2, tx2);
-      fence_proxy_async();
-      mbar_expect_tx(smem_u32(&bars[s]), TILE_BYTES);
-      tma_load_3d(smem_u32(ring + s * TILE_BYTES), &tmap, tx2 * TILE_W, ty2 * TILE_H, img2,
-                  smem_u32(&bars[s]));
-    }
-    if (++s == STAGES) {
-      s = 0;
-      parity ^= 1u;
-    }
-  }
+  const WarpSched ws{(int64_t)blockIdx.x * WARPS + warp, (int64_t)gridDim.x * WARPS, p.tiles, p.cshift};
+  tma_ring_loop(&tmap, ws, p.geo, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
+    tile_forward<OUT>(tile, lane, p, img, ty, tx);
+  });
 }
 
 // ------------------------------------------------------------------------------------------

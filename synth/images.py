@@ -119,29 +119,29 @@ def device_uniform(n: int, h: int, w: int, seed: int = 0, device="cuda"):
     return out
 
 
-def _device_sinusoids(torch, g, m: int, h: int, w: int, device):
-    """m fields of 128 + sum of 8 separable-expanded sinusoids (rank-2 outer products)."""
+def _device_sinusoid_field(torch, rng: np.random.Generator, h: int, w: int, device):
+    """128 + sum of 8 sinusoids (parameters from the host rng) as a rank-16 product on the device."""
+    fx, fy = rng.uniform(0.0, 0.1, 8), rng.uniform(0.0, 0.1, 8)
+    ph, amp = rng.uniform(0.0, 2 * math.pi, 8), rng.uniform(4.0, 16.0, 8)
     two_pi = 2 * math.pi
-    fx = torch.rand((m, 8), generator=g, device=device, dtype=torch.float64) * 0.1
-    fy = torch.rand((m, 8), generator=g, device=device, dtype=torch.float64) * 0.1
-    ph = torch.rand((m, 8), generator=g, device=device, dtype=torch.float64) * two_pi
-    amp = 4.0 + 12.0 * torch.rand((m, 8), generator=g, device=device, dtype=torch.float64)
     y = torch.arange(h, device=device, dtype=torch.float64)
     x = torch.arange(w, device=device, dtype=torch.float64)
-    ay = two_pi * fy[:, :, None] * y[None, None, :] + ph[:, :, None]   # [m, 8, h]
-    bx = two_pi * fx[:, :, None] * x[None, None, :]                     # [m, 8, w]
-    # sin(a + b) = sin a cos b + cos a sin b  -> two batched rank-8 products
-    U = torch.cat([amp[:, :, None] * torch.sin(ay), amp[:, :, None] * torch.cos(ay)], 1)  # [m,16,h]
-    V = torch.cat([torch.cos(bx), torch.sin(bx)], 1)                                     # [m,16,w]
-    return (128.0 + torch.bmm(U.transpose(1, 2).float(), V.float()))                    # [m, h, w] f32
+    fy_t, fx_t = torch.tensor(fy, device=device), torch.tensor(fx, device=device)
+    ph_t, amp_t = torch.tensor(ph, device=device), torch.tensor(amp, device=device)
+    ay = two_pi * fy_t[:, None] * y[None, :] + ph_t[:, None]          # [8, h]
+    bx = two_pi * fx_t[:, None] * x[None, :]                          # [8, w]
+    # sin(a + b) = sin a cos b + cos a sin b
+    U = torch.cat([amp_t[:, None] * torch.sin(ay), amp_t[:, None] * torch.cos(ay)], 0)  # [16, h]
+    V = torch.cat([torch.cos(bx), torch.sin(bx)], 0)                                   # [16, w]
+    return 128.0 + (U.t().float() @ V.float())                                         # [h, w] f32
 
 
 def device_mixed(n: int, h: int, w: int, seed: int = 0, device="cuda", rect_scale: int = 8,
                  first_index: int = 0, out=None):
     """C5: images of kind (first_index + i) mod 3 (smooth / textured sigma 25 / rectangles).
 
-    Image i depends only on (seed, first_index + i), so any shard of the corpus can be drawn
-    on its own rank without drawing the rest.
+    Image i depends only on (seed, first_index + i), so a rank draws its own shard without the rest.
+    Shape parameters come from a per-image host rng; noise from a per-image device generator.
     """
     torch = _torch()
     if out is None:
@@ -149,20 +149,18 @@ def device_mixed(n: int, h: int, w: int, seed: int = 0, device="cuda", rect_scal
     g = torch.Generator(device=device)
     for i in range(n):
         gi = first_index + i
-        g.manual_seed(seed * 1000003 + gi)
+        rng = np.random.default_rng([seed, gi])
         kind = gi % 3
         if kind == KIND_RECTS:
-            img = torch.empty((h, w), dtype=torch.uint8, device=device)
-            img.fill_(int(torch.randint(0, 256, (1,), generator=g, device=device)))
-            sz = torch.randint(16 * rect_scale, 256 * rect_scale + 1, (24, 2), generator=g, device=device).tolist()
-            for rh, rw in sz:
-                rh, rw = min(rh, h), min(rw, w)
-                y0 = int(torch.randint(0, h - rh + 1, (1,), generator=g, device=device))
-                x0 = int(torch.randint(0, w - rw + 1, (1,), generator=g, device=device))
-                img[y0:y0 + rh, x0:x0 + rw] = int(torch.randint(0, 256, (1,), generator=g, device=device))
-            out[i] = img
+            img = out[i]
+            img.fill_(int(rng.integers(0, 256)))
+            for _ in range(24):
+                rh, rw = (min(int(v), d) for v, d in zip(rng.integers(16 * rect_scale, 256 * rect_scale + 1, 2), (h, w)))
+                y0, x0 = int(rng.integers(0, h - rh + 1)), int(rng.integers(0, w - rw + 1))
+                img[y0:y0 + rh, x0:x0 + rw] = int(rng.integers(0, 256))
         else:
-            f = _device_sinusoids(torch, g, 1, h, w, device)[0]
+            f = _device_sinusoid_field(torch, rng, h, w, device)
+            g.manual_seed(seed * 1000003 + gi)
             sigma = 8.0 if kind == KIND_SMOOTH else 25.0
             f += sigma * torch.randn((h, w), generator=g, device=device, dtype=torch.float32)
             out[i] = f.round_().clamp_(0, 255).to(torch.uint8)
