@@ -136,9 +136,9 @@ void fill_quant_tables(Tables& t, int r, float q) {
 
 template <class K, class P>
 adct_status launch_tma_kernel(K kern, const CUtensorMap& map, const P& params_in, int64_t tiles,
-                              cudaStream_t stream) {
+                              cudaStream_t stream, int stages = STAGES) {
   P params = params_in;
-  const int smem = WARPS * STAGES * TILE_BYTES + WARPS * STAGES * 8;
+  const int smem = WARPS * stages * TILE_BYTES + WARPS * stages * 8;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return cuda_fail(e);
   int dev = 0, sms = 0, occ = 0;
@@ -163,6 +163,12 @@ adct_status launch_tma_kernel(K kern, const CUtensorMap& map, const P& params_in
 }
 
 
+
+// Compress launch: ring depth from the kernel's per-r configuration.
+adct_status launch_compress(CompressKernel kern, int RF, const CUtensorMap& map, const CompressParams& p,
+                            cudaStream_t stream) {
+  return launch_tma_kernel(kern, map, p, p.tiles, stream, compress_stages(RF));
+}
 }  // namespace
 
 extern "C" {
@@ -307,16 +313,16 @@ adct_status adct_compress_psnr(const uint8_t* src, int64_t n, int64_t h, int64_t
   if (e != cudaSuccess) return cuda_fail(e);
   if (q > 0.f) {
     fill_quant_tables(p.tab, r, q);
-    if (recon_t == ADCT_RECON_NONE) return launch_tma_kernel(k_compress<RT, MODE_QUANT, REC_NONE>, map, p, p.tiles, s);
-    if (recon_t == ADCT_RECON_F32) return launch_tma_kernel(k_compress<RT, MODE_QUANT, REC_F32>, map, p, p.tiles, s);
-    return launch_tma_kernel(k_compress<RT, MODE_QUANT, REC_U8>, map, p, p.tiles, s);
+    if (recon_t == ADCT_RECON_NONE) return launch_compress(k_compress<RT, MODE_QUANT, REC_NONE>, RT, map, p, s);
+    if (recon_t == ADCT_RECON_F32) return launch_compress(k_compress<RT, MODE_QUANT, REC_F32>, RT, map, p, s);
+    return launch_compress(k_compress<RT, MODE_QUANT, REC_U8>, RT, map, p, s);
   }
   fill_zonal_tables(p.tab, r);
   if (recon_t == ADCT_RECON_NONE) {
-    return launch_tma_kernel(zonal_kernel(r), map, p, p.tiles, s);
+    return launch_compress(zonal_kernel(r), r, map, p, s);
   }
-  if (recon_t == ADCT_RECON_F32) return launch_tma_kernel(k_compress<RT, MODE_ZONAL, REC_F32>, map, p, p.tiles, s);
-  return launch_tma_kernel(k_compress<RT, MODE_ZONAL, REC_U8>, map, p, p.tiles, s);
+  if (recon_t == ADCT_RECON_F32) return launch_compress(k_compress<RT, MODE_ZONAL, REC_F32>, RT, map, p, s);
+  return launch_compress(k_compress<RT, MODE_ZONAL, REC_U8>, RT, map, p, s);
 }
 
 adct_status adct_psnr(const double* sse, int64_t count, int64_t pixels, double* psnr, adct_stream_t stream) {

@@ -98,20 +98,28 @@ __device__ __forceinline__ void store_recon_row(uint8_t* base, int64_t pitch, in
 }
 
 // ------------------------------------------------------------------------------------------
-// One warp tile (16 rows x 256 columns) of the fused compress path; returns this lane's
-// partial sum of (576 x - 576 x^)^2 for its two blocks (fp32 pair).
+// Fused compress path, split in two halves so that a warp can overlap the ALU-heavy forward of
+// tile j+1 (SWAR IADD3/PRMT) with the FMA-heavy inverse + error of tile j (FADD2/FFMA2) in one
+// basic block: ptxas interleaves the two independent streams and both pipes stay busy.
 // ------------------------------------------------------------------------------------------
-template <int R, int MODE, int RECON>
-__device__ __forceinline__ float2 tile_compress(const uint8_t* tile, int lane, const CompressParams& p,
-                                                int img, int ty, int tx) {
+
+// Forward half: packed SWAR coefficients Y (bias 0x80008000) of the two blocks of this lane.
+template <int R, int MODE>
+__device__ __forceinline__ void compress_fwd(const uint8_t* tile, int lane, uint32_t (&Y)[8][8]) {
   constexpr int RF = (MODE == MODE_QUANT) ? RT : R;  // forward pruning level
   uint32_t P[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
     pack_rows(lds64(tile + i * TILE_W + lane * 8), lds64(tile + (i + 8) * TILE_W + lane * 8), P[i]);
-  uint32_t Y[8][8];
   fwd2d<BIAS2, RF>(P, Y);
+}
 
+// Inverse half: zonal weights / quantiser, inverse with C^T, error against the staged pixels.
+// Returns this lane's partial sum of squared errors (576 units for ZONAL) as an fp32 pair.
+template <int R, int MODE, int RECON>
+__device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const uint8_t* tile, int lane,
+                                               const CompressParams& p, int img, int ty, int tx) {
+  constexpr int RF = (MODE == MODE_QUANT) ? RT : R;
   float2 V[64];
   static_for<64>([&](auto KLc) {
     constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
@@ -128,15 +136,17 @@ __device__ __forceinline__ float2 tile_compress(const uint8_t* tile, int lane, c
     }
   });
 
-  float2 acc = f2(0.f);
+  float2 acc[8];  // one accumulator chain per column: 8 short FFMA2 chains instead of one long one
+#pragma unroll
+  for (int n = 0; n < 8; ++n) acc[n] = f2(0.f);
   const int col = tx * TILE_W + lane * 8;
   uint8_t* rbase = nullptr;
   if constexpr (RECON != REC_NONE) rbase = p.recon + (int64_t)img * p.recon_img_stride;
   inverse2d<RF>(V, [&](auto Ic, auto row) {
     constexpr int I = decltype(Ic)::value;
     using cuda::std::get;
-    const uint2 wa = lds64(tile + I * TILE_W + lane * 8);
-    const uint2 wb = lds64(tile + (I + 8) * TILE_W + lane * 8);
+    const uint2 wa = lds64_reload(tile + I * TILE_W + lane * 8);
+    const uint2 wb = lds64_reload(tile + (I + 8) * TILE_W + lane * 8);
     float2 xr[8];
     static_for<8>([&](auto Nc) {
       constexpr int N = decltype(Nc)::value;
@@ -144,35 +154,50 @@ __device__ __forceinline__ float2 tile_compress(const uint8_t* tile, int lane, c
       const float2 y = (MODE == MODE_ZONAL) ? px576(N < 4 ? wa.x : wa.y, N < 4 ? wb.x : wb.y, N & 3)
                                             : px1(N < 4 ? wa.x : wa.y, N < 4 ? wb.x : wb.y, N & 3);
       const float2 e = rsub(y, get<N>(row));
-      acc = f2fma(e, e, acc);
+      acc[N] = f2fma(e, e, acc[N]);
       if constexpr (RECON != REC_NONE) xr[N] = val(get<N>(row));
     });
     if constexpr (RECON != REC_NONE)
       store_recon_row<RECON, (MODE == MODE_ZONAL)>(rbase, p.recon_pitch, p.h, p.w, ty * TILE_H + I, col, xr);
   });
-  return acc;
+  const float2 s01 = f2add(acc[0], acc[1]), s23 = f2add(acc[2], acc[3]);
+  const float2 s45 = f2add(acc[4], acc[5]), s67 = f2add(acc[6], acc[7]);
+  return f2add(f2add(s01, s23), f2add(s45, s67));
 }
 
-template <int R, int MODE, int RECON>
-__global__ void __launch_bounds__(WARPS * 32, 3)
+// ------------------------------------------------------------------------------------------
+// Fused compress kernel: every warp owns a TMA ring of ST stages and runs forward + inverse +
+// error on each tile (one warp tile = 16 rows x 256 columns = one block pair per lane).
+// Ring depth and the minimum resident CTAs per SM (register cap) are tuned per r
+// (tools/microbench/tune_compress.cu): small r is latency/occupancy-sensitive,
+// large r needs the registers.
+// ------------------------------------------------------------------------------------------
+// measured on B200 (profiles/r01_tune_compress.txt): small r wants occupancy, large r registers
+constexpr int compress_stages(int R) { return 2; }
+constexpr int compress_minb(int R) { return R <= 6 ? 5 : (R <= 24 ? 4 : 3); }
+
+template <int R, int MODE, int RECON, int ST = compress_stages((MODE == MODE_QUANT) ? RT : R),
+          int MINB = (MODE == MODE_ZONAL && RECON == REC_NONE) ? compress_minb(R) : 3>
+__global__ void __launch_bounds__(WARPS * 32, MINB)
     k_compress(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CompressParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr double kSseScale = (MODE == MODE_ZONAL) ? 1.0 / 331776.0 : 1.0;  // errors in 576 units (ZONAL)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint8_t* ring = smem + warp * (STAGES * TILE_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * STAGES * TILE_BYTES) + warp * STAGES;
-
+  uint8_t* ring = smem + warp * (ST * TILE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * ST * TILE_BYTES) + warp * ST;
   const WarpSched ws{(int64_t)blockIdx.x * WARPS + warp, (int64_t)gridDim.x * WARPS, p.tiles, p.cshift};
   int cur = -1;
   double acc = 0.0;
-  tma_ring_loop(&tmap, ws, p.geo, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
+  tma_ring_loop<ST>(&tmap, ws, p.geo, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {  // warp-uniform: flush the finished image's partial SSE
       const double v = warp_sum(acc);
       if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v * kSseScale);
       cur = img;
       acc = 0.0;
     }
-    const float2 e2 = tile_compress<R, MODE, RECON>(tile, lane, p, img, ty, tx);
+    uint32_t Y[8][8];
+    compress_fwd<R, MODE>(tile, lane, Y);
+    const float2 e2 = compress_inv<R, MODE, RECON>(Y, tile, lane, p, img, ty, tx);
     acc += (double)e2.x + (double)e2.y;
   });
   const double v = warp_sum(acc);

@@ -1,0 +1,127 @@
+// TMA streaming microbenchmark: per-warp mbarrier ring of uint8 tiles (box BW x BH) over a
+// [n][h][w] tensor, minimal consumer (one LDS per lane per row). Measures achievable read GB/s
+// for ring depth / box shape / warps per CTA, to separate TMA/DRAM limits from compute limits.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tma_stream tma_stream.cu
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int BW, int BH, int ST, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32) k_stream(const __grid_constant__ CUtensorMap map, int64_t tiles,
+                                                       int tiles_x, int tiles_y, uint32_t* out, int spin) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int TB = BW * BH;
+  uint8_t* ring = smem + warp * ST * TB;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * ST * TB) + warp * ST;
+  const int64_t g = (int64_t)blockIdx.x * WARPS + warp, G = (int64_t)gridDim.x * WARPS;
+  auto coords = [&](int64_t t, int& x, int& y, int& z) {
+    int64_t per = (int64_t)tiles_x * tiles_y;
+    z = (int)(t / per);
+    int64_t r = t - z * per;
+    y = (int)(r / tiles_x) * BH;
+    x = (int)(r % tiles_x) * BW;
+  };
+  auto issue = [&](int s, int64_t t) {
+    int x, y, z;
+    coords(t, x, y, z);
+    uint32_t bar = smem_u32(&bars[s]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(TB) : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(ring + s * TB)),
+        "l"((uint64_t)&map), "r"(x), "r"(y), "r"(z), "r"(bar)
+        : "memory");
+  };
+  if (lane == 0) {
+    for (int s = 0; s < ST; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < ST; ++s)
+      if (g + s * G < tiles) issue(s, g + s * G);
+  }
+  __syncwarp();
+  uint32_t acc = 0;
+  int s = 0;
+  uint32_t par = 0;
+  for (int64_t t = g; t < tiles; t += G) {
+    uint32_t bar = smem_u32(&bars[s]), ok = 0;
+    while (!ok)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p; }"
+                   : "=r"(ok) : "r"(bar), "r"(par) : "memory");
+    for (int i = 0; i < BH; ++i) acc += *reinterpret_cast<const uint32_t*>(ring + s * TB + i * BW + (lane * 4) % BW);
+    for (int k = 0; k < spin; ++k) acc = acc * 1664525u + 1013904223u;
+    __syncwarp();
+    if (lane == 0 && t + ST * G < tiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(s, t + ST * G);
+    }
+    if (++s == ST) { s = 0; par ^= 1; }
+  }
+  if (acc == 0x12345678u) out[0] = acc;
+}
+
+typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                          const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+template <int BW, int BH, int ST, int WARPS>
+void run(uint8_t* d, int n, int h, int w, uint32_t* out, int sms, int spin) {
+  void* p;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+  EncFn enc = (EncFn)p;
+  CUtensorMap map;
+  cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t str[2] = {(cuuint64_t)w, (cuuint64_t)w * h};
+  cuuint32_t box[3] = {BW, BH, 1}, es[3] = {1, 1, 1};
+  enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, d, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  int smem = WARPS * ST * BW * BH + WARPS * ST * 8;
+  auto k = k_stream<BW, BH, ST, WARPS>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, WARPS * 32, smem);
+  int tx = w / BW, ty = h / BH;
+  int64_t tiles = (int64_t)n * tx * ty;
+  int grid = sms * occ;
+  k<<<grid, WARPS * 32, smem>>>(map, tiles, tx, ty, out, spin);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  for (int i = 0; i < 5; ++i) k<<<grid, WARPS * 32, smem>>>(map, tiles, tx, ty, out, spin);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  ms /= 5;
+  double bytes = (double)n * h * w;
+  printf("box %3dx%-3d stages %d warps/cta %d occ %d spin %4d: %7.3f ms  %7.0f GB/s  err=%s\n", BW, BH, ST, WARPS, occ,
+         spin, ms, bytes / ms / 1e6, cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  int sms;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  int n = 256, h = 4096, w = 4096;
+  uint8_t* d;
+  uint32_t* out;
+  cudaMalloc(&d, (size_t)n * h * w);
+  cudaMalloc(&out, 64);
+  cudaMemset(d, 1, (size_t)n * h * w);
+  run<256, 16, 3, 4>(d, n, h, w, out, sms, 0);
+  run<256, 16, 4, 4>(d, n, h, w, out, sms, 0);
+  run<256, 16, 8, 4>(d, n, h, w, out, sms, 0);
+  run<256, 32, 4, 4>(d, n, h, w, out, sms, 0);
+  run<256, 64, 2, 4>(d, n, h, w, out, sms, 0);
+  run<256, 16, 4, 8>(d, n, h, w, out, sms, 0);
+  run<128, 32, 4, 4>(d, n, h, w, out, sms, 0);
+  run<256, 16, 3, 4>(d, n, h, w, out, sms, 200);
+  run<256, 16, 3, 4>(d, n, h, w, out, sms, 400);
+  run<256, 16, 4, 4>(d, n, h, w, out, sms, 400);
+  run<256, 16, 4, 4>(d, n, h, w, out, sms, 800);
+  return 0;
+}

@@ -1,0 +1,107 @@
+// Tuning sweep for the fused compress kernel: ring depth ST, register cap (min CTAs/SM) and
+// chunk size per r, on 256 x 4096^2 random bytes with real TMA traffic.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr
+//        -I../../include -I../../paper_1402_6034_b200/csrc -o tune_compress tune_compress.cu
+#include <cstdio>
+#include <cstring>
+#include "adct_kernels.cuh"
+
+using namespace adct;
+
+typedef CUresult (*EncFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                          const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                          CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static CUtensorMap g_map;
+static uint8_t* g_src;
+static double* g_sse;
+static int g_sms;
+static const int N = 256, H = 4096, W = 4096;
+
+template <int R, int ST, int MINB>
+void run(int cshift_max = 4) {
+  auto k = k_compress<R, MODE_ZONAL, REC_NONE, ST, MINB>;
+  CompressParams p;
+  memset(&p, 0, sizeof(p));
+  p.geo.tiles_x = W / TILE_W;
+  p.geo.tiles_y = H / TILE_H;
+  p.geo.per_img = p.geo.tiles_x * p.geo.tiles_y;
+  p.tiles = p.geo.per_img * N;
+  p.h = H;
+  p.w = W;
+  p.sse = g_sse;
+  for (int kl = 0; kl < 64; ++kl) {
+    float w = zz_index(kl / 8, kl % 8) < R ? (float)wval(kl / 8, kl % 8) : 0.f;
+    p.tab.w[kl] = make_float2(w, w);
+    p.tab.c[kl] = make_float2(-KF * w, -KF * w);
+  }
+  int smem = WARPS * ST * TILE_BYTES + WARPS * ST * 8;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, WARPS * 32, smem);
+  int grid = g_sms * occ;
+  int cshift = cshift_max;
+  while (cshift > 0 && (p.tiles >> cshift) < 2LL * grid * WARPS) --cshift;
+  p.cshift = cshift;
+  k<<<grid, WARPS * 32, smem>>>(g_map, p);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  for (int i = 0; i < 5; ++i) k<<<grid, WARPS * 32, smem>>>(g_map, p);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  ms /= 5;
+  double gbs = (double)N * H * W / ms / 1e6;
+  printf("r=%2d ST=%d MINB=%d occ=%d cshift=%d: %.3f ms %6.0f GB/s frac %.3f %s\n", R, ST, MINB, occ, cshift, ms, gbs,
+         gbs / 6534.1, cudaGetErrorString(cudaGetLastError()));
+  fflush(stdout);
+}
+
+template <int R>
+void sweep() {
+  run<R, 2, 4>();
+  run<R, 3, 4>();
+  run<R, 4, 3>();
+  run<R, 3, 3>();
+  run<R, 2, 3>();
+  run<R, 2, 5>();
+  run<R, 3, 4>(2);
+  run<R, 3, 4>(0);
+}
+
+int main() {
+  cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaMalloc(&g_src, (size_t)N * H * W);
+  cudaMalloc(&g_sse, N * sizeof(double));
+  // pseudo-random bytes
+  {
+    uint8_t* h = (uint8_t*)malloc((size_t)H * W);
+    uint32_t s = 12345;
+    for (size_t i = 0; i < (size_t)H * W; ++i) {
+      s = s * 1664525u + 1013904223u;
+      h[i] = (uint8_t)(s >> 24);
+    }
+    for (int i = 0; i < N; ++i) cudaMemcpy(g_src + (size_t)i * H * W, h, (size_t)H * W, cudaMemcpyHostToDevice);
+    free(h);
+  }
+  void* fp;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
+  cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t str[2] = {(cuuint64_t)W, (cuuint64_t)W * H};
+  cuuint32_t box[3] = {TILE_W, TILE_H, 1}, es[3] = {1, 1, 1};
+  ((EncFn)fp)(&g_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, g_src, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  sweep<1>();
+  sweep<3>();
+  sweep<6>();
+  sweep<10>();
+  sweep<15>();
+  sweep<21>();
+  sweep<28>();
+  sweep<36>();
+  return 0;
+}
