@@ -7,8 +7,9 @@ Workload (BASELINE.json configs[4], "C5", the large-batch configuration the metr
 target is quoted on; it fits one GPU): 4096 uint8 4096x4096 images (64 GiB) of mixed generator
 kinds, zonal compression for r in {1, 3, 6, 10, 15, 21, 28, 36}: per r, forward + zonal mask +
 inverse + per-image SSE (adct_compress_psnr), then an NCCL all-reduce of the per-image SSE
-[8 x 4096] (N > 1) and the PSNR epilogue (adct_psnr).  Images are sharded over ranks (strong
-scaling: the total work is fixed).  One step = all 8 r-passes over the whole corpus.
+[8 x 4096 N] (N > 1) and the PSNR epilogue (adct_psnr).  Each rank processes its own C5-sized
+shard of 4096 images (weak scaling: independent images, per-GPU work fixed as N grows).  One step =
+all 8 r-passes over every rank's images.
 
 Prints ONE JSON line (rank 0).  `value` = total pixel-passes / max-over-ranks device time, in
 Gpixel/s; `e2e` = the same metric through adct_compress_psnr_host (pinned host images, H2D copy
@@ -21,7 +22,6 @@ from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
 import sys
@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["adct", "reference"], default="adct")
-    ap.add_argument("--images", type=int, default=N_IMAGES, help="total images (default: C5's 4096)")
+    ap.add_argument("--images", type=int, default=N_IMAGES,
+                    help="images per rank (default: C5's 4096 = 64 GiB per GPU; weak scaling)")
     ap.add_argument("--e2e-images", type=int, default=64, help="images per rank in the e2e run")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fwd-only", action="store_true")
@@ -163,7 +164,7 @@ def run_reference(a, rank):
     sample = "1 C5 image 4096x4096 x 8 r per step (kinds cycle 0..2), oracle float64 numpy"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": wall / a.steps * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": WORKLOAD, "sample": sample},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -184,6 +185,7 @@ def main():
     import torch.distributed as dist
 
     import paper_1402_6034_b200 as A
+    from paper_1402_6034_b200.dist import combine_sse, max_over_ranks, shard_range
     from synth import images as S
 
     A.load()
@@ -191,8 +193,8 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    n_total = a.images
-    lo, hi = rank * n_total // world, (rank + 1) * n_total // world
+    n_total = a.images * world  # weak scaling: every rank processes a full C5 corpus of its own
+    lo, hi = shard_range(n_total, rank, world)
     n_loc = hi - lo
 
     # ---- inputs: this rank's shard, generated on its own GPU (untimed)
@@ -210,8 +212,7 @@ def main():
             A.compress_psnr(x, r, sse=sse[k, lo:hi])
             if evs is not None:
                 evs[k][1].record(stream)
-        if world > 1:
-            dist.all_reduce(sse)
+        combine_sse(sse)  # the one collective: NCCL all-reduce of the per-image SSE (N > 1)
         A.psnr(sse, H * W, out=psnr)
 
     for _ in range(a.warmup):
@@ -234,13 +235,8 @@ def main():
     ms = t_start.elapsed_time(t_end)
     per_r = [statistics.mean(evs[s][k][0].elapsed_time(evs[s][k][1]) for s in range(a.steps))
              for k in range(len(R_SET))]
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        pr = torch.tensor(per_r, dtype=torch.float64, device=dev)
-        dist.all_reduce(pr, op=dist.ReduceOp.MAX)
-        per_r = pr.tolist()
+    ms = max_over_ranks(ms, dev)
+    per_r = [max_over_ranks(t, dev) for t in per_r]
     ms_step = ms / a.steps
     value = n_total * H * W * len(R_SET) / (ms_step * 1e-3) / 1e9
 
@@ -282,11 +278,7 @@ def main():
         A.compress_psnr_host(host_imgs, R_SET, dev_buf=dev_buf, dev_sse=dev_sse, host_psnr=host_psnr)
     e1.record(stream)
     torch.cuda.synchronize()
-    ems = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ems], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ems = float(t.item())
+    ems = max_over_ranks(e0.elapsed_time(e1), dev)
     e2e = {"value": world * ne * H * W * len(R_SET) / (ems / e_steps * 1e-3) / 1e9, "unit": UNIT,
            "h2d_bytes_per_step": ne * H * W, "d2h_bytes_per_step": len(R_SET) * ne * 8,
            "images_per_rank": ne, "api": "adct_compress_psnr_host"}
@@ -317,10 +309,11 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-                "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "u8->i16x2(int32 SWAR)/f32x2", "data": "synthetic",
-                "config": {"workload": WORKLOAD, "images": n_total, "h": H, "w": W, "r": list(R_SET),
-                           "parallelism": f"dp{world} (images sharded, NCCL all-reduce of SSE)",
+                "config": {"workload": WORKLOAD, "images": n_total, "images_per_gpu": n_loc, "h": H, "w": W,
+                           "r": list(R_SET),
+                           "parallelism": f"dp{world} (images sharded; one NCCL all-reduce of per-image SSE)",
                            "l2": "inputs 64 GiB >> 126 MB L2 (no flush needed)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "fwd_only_c3": fwd_only,

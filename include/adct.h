@@ -133,6 +133,14 @@ adct_status adct_compress_psnr_host(const uint8_t* host_src, int64_t n, int64_t 
                                     int64_t dev_buf_bytes, double* dev_sse, double* host_psnr,
                                     adct_stream_t stream);
 
+/*
+ * adct_quant_reciprocals — HOST helper, no device work: the 64 per-position fp32 constants c'
+ * the QUANT kernels use (c' = smallest fp32 strictly above 1/(q sqrt(d_k d_l)), raster order
+ * k*8+l), so that the quantiser decision round-to-nearest(Y c') can be audited on the CPU.
+ *   c_out  host float[64].  ADCT_EINVAL if q <= 0, NaN or inf, or c_out is NULL.
+ */
+adct_status adct_quant_reciprocals(float q, float* c_out);
+
 /* Human-readable status; static storage. */
 const char* adct_status_string(adct_status s);
 /* cudaError_t of the last ADCT_ECUDA on this thread (0 if none). */

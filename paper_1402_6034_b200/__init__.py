@@ -4,7 +4,7 @@ Python surface = the C ABI in include/adct.h (same names, argument marshalling o
 forward, inverse, compress_psnr, psnr, compress_psnr_host.  See DESIGN.md.
 """
 from ._lib import (AdctError, compress_psnr, compress_psnr_host, empty_plane, forward, inverse,  # noqa: F401
-                   launch_count, load, psnr, to_device, version)
+                   launch_count, load, psnr, quant_reciprocals, to_device, version)
 
 __all__ = ["forward", "inverse", "compress_psnr", "psnr", "compress_psnr_host", "load", "launch_count",
-           "version", "AdctError", "empty_plane", "to_device"]
+           "version", "AdctError", "empty_plane", "to_device", "quant_reciprocals"]

@@ -28,6 +28,7 @@ SIGNATURES = {
     "adct_psnr": (_i32, [_vp, _i64, _i64, _vp, _vp]),
     "adct_compress_psnr_host": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _i32, _f32, _vp, _i64,
                                        _vp, _vp, _vp]),
+    "adct_quant_reciprocals": (_i32, [_f32, _vp]),
     "adct_status_string": (ctypes.c_char_p, [_i32]),
     "adct_last_cuda_error": (_i32, []),
     "adct_version": (_i32, []),
@@ -109,6 +110,13 @@ def to_device(x, device="cuda"):
     out = empty_plane(*t.shape, dtype=t.dtype, device=device)
     out.copy_(t)
     return out
+
+
+def quant_reciprocals(q: float) -> np.ndarray:
+    """adct_quant_reciprocals: the kernels' per-position quantiser constants c' (host, no GPU)."""
+    out = np.zeros(64, dtype=np.float32)
+    _check(load().adct_quant_reciprocals(float(q), out.ctypes.data), "adct_quant_reciprocals")
+    return out.reshape(8, 8)
 
 
 def launch_count() -> int:

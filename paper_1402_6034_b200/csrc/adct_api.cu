@@ -325,6 +325,13 @@ adct_status adct_compress_psnr(const uint8_t* src, int64_t n, int64_t h, int64_t
   return launch_compress(k_compress<RT, MODE_ZONAL, REC_U8>, RT, map, p, s);
 }
 
+adct_status adct_quant_reciprocals(float q, float* c_out) {
+  if (!c_out || !(q > 0.f) || isinf(q)) return ADCT_EINVAL;
+  for (int k = 0; k < 8; ++k)
+    for (int l = 0; l < 8; ++l) c_out[k * 8 + l] = quant_recip(q, dval(k) * dval(l));
+  return ADCT_OK;
+}
+
 adct_status adct_psnr(const double* sse, int64_t count, int64_t pixels, double* psnr, adct_stream_t stream) {
   if (!sse || !psnr || count < 1 || pixels < 1) return ADCT_EINVAL;
   if (((uintptr_t)sse & 7u) || ((uintptr_t)psnr & 7u)) return ADCT_EALIGN;
