@@ -115,6 +115,11 @@ float quant_recip(float q, int dd) {
 void fill_zonal_tables(Tables& t, int r) {
   for (int k = 0; k < 8; ++k)
     for (int l = 0; l < 8; ++l) {
+      t.wc[wclass(k, l)] = (float)wval(k, l);
+      t.cc[wclass(k, l)] = -KF * (float)wval(k, l);
+    }
+  for (int k = 0; k < 8; ++k)
+    for (int l = 0; l < 8; ++l) {
       const bool keep = zz_host(k, l) < r;
       const float w = keep ? (float)wval(k, l) : 0.f;
       t.w[k * 8 + l] = make_float2(w, w);

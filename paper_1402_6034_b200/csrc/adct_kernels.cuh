@@ -19,7 +19,15 @@ enum { MODE_ZONAL = 0, MODE_QUANT = 1 };
 enum { OUT_I16 = 0, OUT_I32 = 1, OUT_F32 = 2 };
 enum { REC_NONE = 0, REC_F32 = 1, REC_U8 = 2 };
 
+// weight class of position (k, l): d_k d_l in {64, 48, 32, 36, 24, 16} -> 0..5
+constexpr int wclass(int k, int l) {
+  const int dd = dval(k) * dval(l);
+  return dd == 64 ? 0 : dd == 48 ? 1 : dd == 32 ? 2 : dd == 36 ? 3 : dd == 24 ? 4 : 5;
+}
+
 struct Tables {
+  float wc[8];   // ZONAL compile-time r: W per weight class (loop-invariant, uniform registers)
+  float cc[8];   // ZONAL compile-time r: -KF * W per weight class
   float2 w[64];  // ZONAL: (W, W); QUANT: q / sqrt(d_k d_l); INVERSE: per-coef scale — 0 where masked
   float2 c[64];  // ZONAL: (-KF W, -KF W) [masked: 0]; QUANT: (c', c') quantiser reciprocal
 };
@@ -124,8 +132,13 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
   static_for<64>([&](auto KLc) {
     constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
     if constexpr (kept(RF, k, l)) {
-      if constexpr (MODE == MODE_ZONAL) {
-        V[kl] = f2fma(biased_pair(Y[k][l]), p.tab.w[kl], p.tab.c[kl]);  // W . M . Y, exact
+      if constexpr (MODE == MODE_ZONAL && RF < RT) {
+        // scalar weight / offset broadcast to both lanes from 12 loop-invariant class constants:
+        // an FFMA2 that reads three distinct register pairs issues at 1/3 rate on B200
+        constexpr int c = wclass(k, l);
+        V[kl] = f2fma(biased_pair(Y[k][l]), f2(p.tab.wc[c]), f2(p.tab.cc[c]));  // W . M . Y, exact
+      } else if constexpr (MODE == MODE_ZONAL) {
+        V[kl] = f2fma(biased_pair(Y[k][l]), f2(p.tab.w[kl].x), f2(p.tab.c[kl].x));  // runtime mask in w
       } else {
         const float2 y = f2add(biased_pair(Y[k][l]), f2(-KF));          // Y, exact
         // 1.5*2^23 + RN(Y c'): c' lies strictly above 1/(q sqrt dd), so exact ties of Z/q round
@@ -176,8 +189,11 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
 constexpr int compress_stages(int R) { return 2; }
 constexpr int compress_minb(int R) { return R <= 6 ? 5 : (R <= 24 ? 4 : 3); }
 
+constexpr int compress_prefetch(int R) { return 0; }
+
 template <int R, int MODE, int RECON, int ST = compress_stages((MODE == MODE_QUANT) ? RT : R),
-          int MINB = (MODE == MODE_ZONAL && RECON == REC_NONE) ? compress_minb(R) : 3>
+          int MINB = (MODE == MODE_ZONAL && RECON == REC_NONE) ? compress_minb(R) : 3,
+          int PF = compress_prefetch(R)>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     k_compress(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CompressParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -188,7 +204,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
   const WarpSched ws{(int64_t)blockIdx.x * WARPS + warp, (int64_t)gridDim.x * WARPS, p.tiles, p.cshift};
   int cur = -1;
   double acc = 0.0;
-  tma_ring_loop<ST>(&tmap, ws, p.geo, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
+  tma_ring_loop<ST, PF>(&tmap, ws, p.geo, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {  // warp-uniform: flush the finished image's partial SSE
       const double v = warp_sum(acc);
       if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v * kSseScale);

@@ -25,23 +25,26 @@ __global__ void __launch_bounds__(128, MIN_CTAS) k_body(const uint8_t* src, Comp
 }
 
 template <int R, int MIN_CTAS>
-void run(const uint8_t* src, float* out, int sms) {
+void run(const uint8_t* src, float* out, int sms, int dyn_smem = 0) {
   CompressParams p;
   memset(&p, 0, sizeof(p));
   for (int k = 0; k < 64; ++k) {
     float w = (float)wval(k / 8, k % 8);
+    p.tab.wc[wclass(k / 8, k % 8)] = w;
+    p.tab.cc[wclass(k / 8, k % 8)] = -KF * w;
     p.tab.w[k] = make_float2(w, w);
     p.tab.c[k] = make_float2(-KF * w, -KF * w);
   }
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_body<R, MIN_CTAS>, 128, 0);
+  cudaFuncSetAttribute(k_body<R, MIN_CTAS>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_body<R, MIN_CTAS>, 128, dyn_smem);
   int grid = sms * occ, iters = 2000;
-  k_body<R, MIN_CTAS><<<grid, 128>>>(src, p, 10, out);
+  k_body<R, MIN_CTAS><<<grid, 128, dyn_smem>>>(src, p, 10, out);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   cudaEventRecord(a);
-  k_body<R, MIN_CTAS><<<grid, 128>>>(src, p, iters, out);
+  k_body<R, MIN_CTAS><<<grid, 128, dyn_smem>>>(src, p, iters, out);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
@@ -62,12 +65,12 @@ int main() {
   uint8_t h[65536];
   for (int i = 0; i < 65536; ++i) h[i] = (uint8_t)((i * 2654435761u) >> 13);
   cudaMemcpy(src, h, 65536, cudaMemcpyHostToDevice);
-  run<1, 4>(src, out, sms);
-  run<3, 4>(src, out, sms);
-  run<10, 3>(src, out, sms);
-  run<21, 3>(src, out, sms);
+  run<1, 5>(src, out, sms);
+  run<1, 5>(src, out, sms, 30000);   // 5 CTAs (smem-limited like the real kernel)
+  run<1, 5>(src, out, sms, 60000);   // 3 CTAs
+  run<10, 4>(src, out, sms);
+  run<10, 4>(src, out, sms, 40000);
   run<36, 3>(src, out, sms);
-  run<1, 2>(src, out, sms);
-  run<36, 2>(src, out, sms);
+  run<36, 3>(src, out, sms, 100000);
   return 0;
 }

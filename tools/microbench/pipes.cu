@@ -48,6 +48,17 @@ __global__ void __launch_bounds__(256) kern(uint32_t* out, uint32_t seed, unsign
       if (OP == 11) asm volatile("mad.wide.s32 %0, %1, %1, %0;" : "+l"(rr[c]) : "r"(r[c]));
       if (OP == 12) asm volatile("add.f32 %0, %0, 0f3F800000;" : "+r"(r[c]));
       if (OP == 13) asm volatile("fma.rn.f32 %0, %0, 0f3F800001, 0f3F800000;" : "+r"(r[c]));
+      // live-operand variants: every source is a distinct, changing register
+      if (OP == 14) asm volatile("{.reg .s32 t; add.s32 t, %0, %1; add.s32 %0, t, %2;}" : "+r"(r[c]) : "r"(r[(c + 1) % CH]), "r"(r[(c + 3) % CH]));
+      if (OP == 15) asm volatile("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(rr[c]) : "l"(rr[(c + 1) % CH]), "l"(rr[(c + 3) % CH]));
+      if (OP == 16) asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(rr[c]) : "l"(rr[(c + 1) % CH]));
+      if (OP == 17) asm volatile("prmt.b32 %0, %0, %1, 0x5140;" : "+r"(r[c]) : "r"(r[(c + 1) % CH]));
+      if (OP == 18) {  // the compress mix: 3-input IADD3 + FADD2 + PRMT + FFMA2, all live operands
+        asm volatile("{.reg .s32 t; add.s32 t, %0, %1; add.s32 %0, t, %2;}" : "+r"(r[c]) : "r"(r[(c + 1) % CH]), "r"(r[(c + 3) % CH]));
+        asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(rr[c]) : "l"(rr[(c + 1) % CH]));
+        asm volatile("prmt.b32 %0, %0, %1, 0x5140;" : "+r"(f[c]) : "r"(r[(c + 2) % CH]));
+        asm volatile("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(rr[(c + 4) % CH]) : "l"(rr[(c + 5) % CH]), "l"(rr[(c + 6) % CH]));
+      }
     }
   }
   unsigned long long t1 = clock64();
@@ -106,5 +117,10 @@ int main() {
   run<7>("ffma2", 2, 1, sms);
   run<8>("iadd+fadd2", 1, 2, sms);
   run<9>("iadd+fadd", 1, 2, sms);
+  run<14>("iadd3 live", 1, 1, sms);
+  run<15>("ffma2 live", 2, 1, sms);
+  run<16>("fadd2 live", 2, 1, sms);
+  run<17>("prmt live", 1, 1, sms);
+  run<18>("mix4 live", 1, 4, sms);
   return 0;
 }

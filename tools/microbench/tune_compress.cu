@@ -18,9 +18,9 @@ static double* g_sse;
 static int g_sms;
 static const int N = 256, H = 4096, W = 4096;
 
-template <int R, int ST, int MINB>
+template <int R, int ST, int MINB, int PF = 0>
 void run(int cshift_max = 4) {
-  auto k = k_compress<R, MODE_ZONAL, REC_NONE, ST, MINB>;
+  auto k = k_compress<R, MODE_ZONAL, REC_NONE, ST, MINB, PF>;
   CompressParams p;
   memset(&p, 0, sizeof(p));
   p.geo.tiles_x = W / TILE_W;
@@ -31,6 +31,8 @@ void run(int cshift_max = 4) {
   p.w = W;
   p.sse = g_sse;
   for (int kl = 0; kl < 64; ++kl) {
+    p.tab.wc[wclass(kl / 8, kl % 8)] = (float)wval(kl / 8, kl % 8);
+    p.tab.cc[wclass(kl / 8, kl % 8)] = -KF * (float)wval(kl / 8, kl % 8);
     float w = zz_index(kl / 8, kl % 8) < R ? (float)wval(kl / 8, kl % 8) : 0.f;
     p.tab.w[kl] = make_float2(w, w);
     p.tab.c[kl] = make_float2(-KF * w, -KF * w);
@@ -55,21 +57,15 @@ void run(int cshift_max = 4) {
   cudaEventElapsedTime(&ms, a, b);
   ms /= 5;
   double gbs = (double)N * H * W / ms / 1e6;
-  printf("r=%2d ST=%d MINB=%d occ=%d cshift=%d: %.3f ms %6.0f GB/s frac %.3f %s\n", R, ST, MINB, occ, cshift, ms, gbs,
+  printf("r=%2d ST=%d MINB=%d PF=%d occ=%d cshift=%d: %.3f ms %6.0f GB/s frac %.3f %s\n", R, ST, MINB, PF, occ, cshift, ms, gbs,
          gbs / 6534.1, cudaGetErrorString(cudaGetLastError()));
   fflush(stdout);
 }
 
-template <int R>
+template <int R, int MB>
 void sweep() {
-  run<R, 2, 4>();
-  run<R, 3, 4>();
-  run<R, 4, 3>();
-  run<R, 3, 3>();
-  run<R, 2, 3>();
-  run<R, 2, 5>();
-  run<R, 3, 4>(2);
-  run<R, 3, 4>(0);
+  run<R, 2, MB, 0>();
+  run<R, 3, MB - 1, 0>();
 }
 
 int main() {
@@ -95,13 +91,13 @@ int main() {
   cuuint32_t box[3] = {TILE_W, TILE_H, 1}, es[3] = {1, 1, 1};
   ((EncFn)fp)(&g_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, g_src, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  sweep<1>();
-  sweep<3>();
-  sweep<6>();
-  sweep<10>();
-  sweep<15>();
-  sweep<21>();
-  sweep<28>();
-  sweep<36>();
+  sweep<1, 5>();
+  sweep<3, 5>();
+  sweep<6, 5>();
+  sweep<10, 4>();
+  sweep<15, 4>();
+  sweep<21, 4>();
+  sweep<28, 3>();
+  sweep<36, 3>();
   return 0;
 }
