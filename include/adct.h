@@ -134,6 +134,34 @@ adct_status adct_compress_psnr_host(const uint8_t* host_src, int64_t n, int64_t 
                                     adct_stream_t stream);
 
 /*
+ * Dense comparator / variant path: the same block pipeline with an 8x8
+ * transform T applied as dense fp32 matrix products (SSE in fp64) — for the paper's comparison curves
+ * (Fig. 3): the exact DCT, the SDCT, the coarse C0/2, or any caller matrix.
+ *   ADCT_T_PROPOSED  C_orth = S C0 (dense; cross-check of the fast path)
+ *   ADCT_T_DCT       exact orthonormal DCT-II (reading R1)
+ *   ADCT_T_SDCT      sign(C) / (2 sqrt 2) (reading R11; not orthogonal)
+ *   ADCT_T_COARSE    C0 / 2 (not orthogonal)
+ *   ADCT_T_CUSTOM    `custom`: host double[64], row-major
+ * Per block Z = T X T^T, the first r zig-zag coefficients kept, X^ = T^T Z T (the transpose is the
+ * exact inverse for orthogonal T and the approximate inversion otherwise), and
+ * sse[i] = per-image sum of (x - X^)^2 in fp64 (sse: device double[n], overwritten).
+ */
+typedef enum {
+  ADCT_T_PROPOSED = 0,
+  ADCT_T_DCT = 1,
+  ADCT_T_SDCT = 2,
+  ADCT_T_COARSE = 3,
+  ADCT_T_CUSTOM = 4
+} adct_transform_t;
+
+adct_status adct_compress_psnr_dense(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                                     int64_t img_stride, int r, adct_transform_t t, const double* custom,
+                                     double* sse, adct_stream_t stream);
+
+/* HOST helper: the library's own 8x8 matrix for t (ADCT_T_PROPOSED..ADCT_T_COARSE), row-major. */
+adct_status adct_transform_matrix(adct_transform_t t, double* out);
+
+/*
  * adct_quant_reciprocals — HOST helper, no device work: the 64 per-position fp32 constants c'
  * the QUANT kernels use (c' = smallest fp32 strictly above 1/(q sqrt(d_k d_l)), raster order
  * k*8+l), so that the quantiser decision round-to-nearest(Y c') can be audited on the CPU.

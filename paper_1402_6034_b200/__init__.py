@@ -3,8 +3,10 @@
 Python surface = the C ABI in include/adct.h (same names, argument marshalling only):
 forward, inverse, compress_psnr, psnr, compress_psnr_host.  See DESIGN.md.
 """
-from ._lib import (AdctError, compress_psnr, compress_psnr_host, empty_plane, forward, inverse,  # noqa: F401
-                   launch_count, load, psnr, quant_reciprocals, to_device, version)
+from ._lib import (AdctError, compress_psnr, compress_psnr_dense, compress_psnr_host, empty_plane,  # noqa: F401
+                   forward, inverse, launch_count, load, psnr, quant_reciprocals, to_device,
+                   transform_matrix, version)
 
 __all__ = ["forward", "inverse", "compress_psnr", "psnr", "compress_psnr_host", "load", "launch_count",
-           "version", "AdctError", "empty_plane", "to_device", "quant_reciprocals"]
+           "version", "AdctError", "empty_plane", "to_device", "quant_reciprocals",
+           "compress_psnr_dense", "transform_matrix"]

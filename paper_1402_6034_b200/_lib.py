@@ -29,6 +29,8 @@ SIGNATURES = {
     "adct_compress_psnr_host": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _i32, _f32, _vp, _i64,
                                        _vp, _vp, _vp]),
     "adct_quant_reciprocals": (_i32, [_f32, _vp]),
+    "adct_compress_psnr_dense": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _vp, _vp]),
+    "adct_transform_matrix": (_i32, [_i32, _vp]),
     "adct_status_string": (ctypes.c_char_p, [_i32]),
     "adct_last_cuda_error": (_i32, []),
     "adct_version": (_i32, []),
@@ -110,6 +112,31 @@ def to_device(x, device="cuda"):
     out = empty_plane(*t.shape, dtype=t.dtype, device=device)
     out.copy_(t)
     return out
+
+
+TRANSFORMS = {"proposed": 0, "dct": 1, "sdct": 2, "coarse": 3, "custom": 4}
+
+
+def transform_matrix(kind: str) -> np.ndarray:
+    """adct_transform_matrix: the library's own 8x8 matrix (host, no GPU)."""
+    out = np.zeros(64, dtype=np.float64)
+    _check(load().adct_transform_matrix(TRANSFORMS[kind], out.ctypes.data), "adct_transform_matrix")
+    return out.reshape(8, 8)
+
+
+def compress_psnr_dense(x, r: int, transform: str = "dct", matrix=None, sse=None, stream=None):
+    """adct_compress_psnr_dense: the block pipeline with a dense fp64 8x8 transform (comparators)."""
+    torch = _torch()
+    p, n, h, w, pitch, istr = _plane(x, 1)
+    if sse is None:
+        sse = torch.empty((n,), dtype=torch.float64, device=x.device)
+    cm = None
+    if transform == "custom":
+        cm = np.ascontiguousarray(np.asarray(matrix, dtype=np.float64).reshape(64))
+    _check(load().adct_compress_psnr_dense(p, n, h, w, pitch, istr, r, TRANSFORMS[transform],
+                                           cm.ctypes.data if cm is not None else None, sse.data_ptr(),
+                                           _stream(stream)), "adct_compress_psnr_dense")
+    return sse
 
 
 def quant_reciprocals(q: float) -> np.ndarray:

@@ -330,6 +330,77 @@ adct_status adct_compress_psnr(const uint8_t* src, int64_t n, int64_t h, int64_t
   return launch_compress(k_compress<RT, MODE_ZONAL, REC_U8>, RT, map, p, s);
 }
 
+// The library's own matrices (independent of the CPU oracle): exact DCT-II from cos, C0 = [2C]
+// with Matlab rounding, S from diag(C0 C0^T)^(-1/2), SDCT = sign(C)/(2 sqrt 2), coarse = C0 / 2.
+static void build_matrix(adct_transform_t t, double* M) {
+  const double PI = 3.14159265358979323846;
+  double C[64];
+  for (int m = 0; m < 8; ++m)
+    for (int n = 0; n < 8; ++n)
+      C[m * 8 + n] = (m == 0 ? 1.0 / (2.0 * sqrt(2.0)) : 0.5) * cos((2 * n + 1) * m * PI / 16.0);
+  for (int i = 0; i < 64; ++i) {
+    const double twoc = 2.0 * C[i];
+    const double c0 = (twoc < 0 ? -1.0 : 1.0) * floor(fabs(twoc) + 0.5);  // round half away from zero
+    const double sgn = (C[i] > 1e-12) ? 1.0 : (C[i] < -1e-12 ? -1.0 : 0.0);
+    switch (t) {
+      case ADCT_T_DCT: M[i] = C[i]; break;
+      case ADCT_T_SDCT: M[i] = sgn / (2.0 * sqrt(2.0)); break;
+      case ADCT_T_COARSE: M[i] = 0.5 * c0; break;
+      default: M[i] = c0; break;  // PROPOSED: scaled below
+    }
+  }
+  if (t == ADCT_T_PROPOSED) {
+    for (int m = 0; m < 8; ++m) {
+      double d = 0.0;
+      for (int n = 0; n < 8; ++n) d += M[m * 8 + n] * M[m * 8 + n];
+      for (int n = 0; n < 8; ++n) M[m * 8 + n] /= sqrt(d);
+    }
+  }
+}
+
+adct_status adct_transform_matrix(adct_transform_t t, double* out) {
+  if (!out || t < ADCT_T_PROPOSED || t > ADCT_T_COARSE) return ADCT_EINVAL;
+  build_matrix(t, out);
+  return ADCT_OK;
+}
+
+adct_status adct_compress_psnr_dense(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                                     int64_t img_stride, int r, adct_transform_t t, const double* custom,
+                                     double* sse, adct_stream_t stream) {
+  adct_status st = check_geom(n, h, w);
+  if (st) return st;
+  if (r < 1 || r > 64 || !sse) return ADCT_EINVAL;
+  if (t < ADCT_T_PROPOSED || t > ADCT_T_CUSTOM || (t == ADCT_T_CUSTOM && !custom)) return ADCT_EINVAL;
+  if ((st = check_plane(src, h, w, pitch, img_stride))) return st;
+  if ((uintptr_t)sse & 7u) return ADCT_EALIGN;
+  CUtensorMap map;
+  if ((st = make_u8_map(&map, src, n, h, w, pitch, img_stride))) return st;
+  DenseParams p;
+  memset(&p, 0, sizeof(p));
+  p.geo = make_geo(h, w);
+  p.tiles = p.geo.per_img * n;
+  p.h = (int)h;
+  p.w = (int)w;
+  p.sse = sse;
+  for (int k = 0; k < 8; ++k)
+    for (int l = 0; l < 8; ++l)
+      if (zz_host(k, l) < r) p.keep_raster |= 1ull << (k * 8 + l);
+  double Tm[64];
+  if (t == ADCT_T_CUSTOM) {
+    for (int i = 0; i < 64; ++i) {
+      if (!isfinite(custom[i])) return ADCT_EINVAL;
+      Tm[i] = custom[i];
+    }
+  } else {
+    build_matrix(t, Tm);
+  }
+  for (int i = 0; i < 64; ++i) p.T[i] = (float)Tm[i];
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(double) * (size_t)n, s);
+  if (e != cudaSuccess) return cuda_fail(e);
+  return launch_tma_kernel(k_compress_dense<0>, map, p, p.tiles, s);
+}
+
 adct_status adct_quant_reciprocals(float q, float* c_out) {
   if (!c_out || !(q > 0.f) || isinf(q)) return ADCT_EINVAL;
   for (int k = 0; k < 8; ++k)

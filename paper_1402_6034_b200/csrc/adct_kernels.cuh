@@ -352,6 +352,103 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_inverse(const __grid_constant
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Dense comparator path: any 8x8 transform T as dense fp32 products — the
+// exact DCT (the paper's reference curve), the SDCT sign(C)/(2 sqrt2) (P:78,
+// P:288-289), the coarse C0/2 or a caller matrix.  Per block: Z = T X T^T, keep the
+// first r zig-zag coefficients, X^ = T^T Z T (the transpose is the inverse for orthogonal T and
+// the "approximate inversion" otherwise), per-image SSE accumulated in fp64.
+// Column-at-a-time formulation: for each frequency column l,  u = X T[l]^T,  z = T u (column l
+// of Z, masked),  w = T^T z,  X^ += w T[l]  — one 8x8 accumulator live; T read as constant-bank
+// operands; pixels re-read from the staged tile.
+// ------------------------------------------------------------------------------------------
+struct DenseParams {
+  TileGeo geo;
+  int64_t tiles;
+  int cshift;
+  int h, w;
+  double* sse;
+  uint64_t keep_raster;  // bit k*8+l: coefficient (k, l) kept
+  float T[64];           // row-major T[m][n]
+};
+
+__device__ __forceinline__ float px_byte(uint2 wv, int j) {
+  return (float)((j < 4 ? (wv.x >> (8 * j)) : (wv.y >> (8 * (j - 4)))) & 0xFFu);
+}
+
+__device__ __forceinline__ double dense_block_sse(const uint8_t* tile, int lane, int b, const DenseParams& p) {
+  float Xh[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int n = 0; n < 8; ++n) Xh[i][n] = 0.f;
+#pragma unroll
+  for (int l = 0; l < 8; ++l) {
+    float u[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint2 wv = lds64(tile + (b * 8 + i) * TILE_W + lane * 8);
+      float a = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) a = fmaf(px_byte(wv, j), p.T[l * 8 + j], a);
+      u[i] = a;
+    }
+    float z[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      float a = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a = fmaf(p.T[k * 8 + i], u[i], a);
+      z[k] = ((p.keep_raster >> (k * 8 + l)) & 1ull) ? a : 0.f;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float wi = 0.f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) wi = fmaf(p.T[k * 8 + i], z[k], wi);
+#pragma unroll
+      for (int n = 0; n < 8; ++n) Xh[i][n] = fmaf(wi, p.T[l * 8 + n], Xh[i][n]);
+    }
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint2 wv = lds64(tile + (b * 8 + i) * TILE_W + lane * 8);
+    float row = 0.f;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      const float e = px_byte(wv, n) - Xh[i][n];
+      row = fmaf(e, e, row);
+    }
+    acc += (double)row;
+  }
+  return acc;
+}
+
+template <int UNUSED = 0>
+__global__ void __launch_bounds__(WARPS * 32, 3)
+    k_compress_dense(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ DenseParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = smem + warp * (STAGES * TILE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * STAGES * TILE_BYTES) + warp * STAGES;
+  const WarpSched ws{(int64_t)blockIdx.x * WARPS + warp, (int64_t)gridDim.x * WARPS, p.tiles, p.cshift};
+  int cur = -1;
+  double acc = 0.0;
+  tma_ring_loop<STAGES>(&tmap, ws, p.geo, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
+    if (img != cur) {
+      const double v = warp_sum(acc);
+      if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v);
+      cur = img;
+      acc = 0.0;
+    }
+    acc += dense_block_sse(tile, lane, 0, p);
+    acc += dense_block_sse(tile, lane, 1, p);
+  });
+  const double v = warp_sum(acc);
+  if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v);
+}
+
 typedef void (*CompressKernel)(CUtensorMap, CompressParams);
 // zonal kernels k_compress<r, ZONAL, RECON_NONE>, instantiated in zonal_part*.cu (4 TUs)
 CompressKernel zonal_kernel(int r);

@@ -21,7 +21,7 @@ def header_functions():
 def test_library_exports_every_declared_symbol():
     lib = A.load()
     names = header_functions()
-    assert len(names) == 10
+    assert len(names) == 12
     for name in names:
         assert hasattr(lib, name), name
         assert name in _lib.SIGNATURES, name
@@ -112,3 +112,23 @@ def test_product_package_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_library_matrices_match_oracle():
+    """The library builds its own matrices (no shared code); they must equal the oracle's."""
+    import numpy as np
+    import oracle as O
+    assert np.abs(A.transform_matrix("dct") - O.dct_matrix()).max() < 1e-15
+    assert np.abs(A.transform_matrix("proposed") - O.proposed_matrix()).max() < 1e-15
+    assert np.abs(A.transform_matrix("sdct") - O.sdct_matrix()).max() < 1e-15
+    assert np.abs(A.transform_matrix("coarse") - O.coarse_matrix()).max() < 1e-15
+    with pytest.raises(A.AdctError):
+        A.transform_matrix("custom")
+
+
+def test_dense_validation():
+    lib = A.load()
+    E = _lib.ADCT_EINVAL
+    assert lib.adct_compress_psnr_dense(16, 1, 8, 16, 16, 128, 0, 1, None, 64, None) == E     # r = 0
+    assert lib.adct_compress_psnr_dense(16, 1, 8, 16, 16, 128, 10, 4, None, 64, None) == E    # custom w/o matrix
+    assert lib.adct_compress_psnr_dense(16, 1, 8, 16, 16, 128, 10, 9, None, 64, None) == E    # bad enum
