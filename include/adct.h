@@ -158,6 +158,22 @@ adct_status adct_compress_psnr_dense(const uint8_t* src, int64_t n, int64_t h, i
                                      int64_t img_stride, int r, adct_transform_t t, const double* custom,
                                      double* sse, adct_stream_t stream);
 
+/*
+ * Parseval sweep: one read of the images yields the SSE of every triangular r.
+ * Since C is orthogonal, the zonal error of a block equals its discarded orthonormal
+ * energy: 576^2 SSE(r) = 576 sum_{zz >= r} W Y^2.  adct_diag_energy writes, per image, the exact
+ * energies E[i][s] = sum over blocks of sum_{k+l=s} W_kl Y_kl^2, s = 0..14 (energy: device
+ * uint64[n][16], entry 15 unused, overwritten).  adct_sweep_psnr turns them into SSE and PSNR for
+ * every r that ends on a full anti-diagonal, r in {1,3,6,10,15,21,28,36,43,49,54,58,61,63,64}
+ * (host int r_list[n_r], n_r <= 16; other r -> ADCT_EINVAL):
+ * sse / psnr device double[n_r][n].  No inverse transform is computed: this is a separate mode,
+ * not the fwd+zonal+inv path.
+ */
+adct_status adct_diag_energy(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                             int64_t img_stride, uint64_t* energy, adct_stream_t stream);
+adct_status adct_sweep_psnr(const uint64_t* energy, int64_t n, int64_t pixels, const int* r_list, int n_r,
+                            double* sse, double* psnr, adct_stream_t stream);
+
 /* HOST helper: the library's own 8x8 matrix for t (ADCT_T_PROPOSED..ADCT_T_COARSE), row-major. */
 adct_status adct_transform_matrix(adct_transform_t t, double* out);
 

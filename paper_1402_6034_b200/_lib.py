@@ -31,6 +31,8 @@ SIGNATURES = {
     "adct_quant_reciprocals": (_i32, [_f32, _vp]),
     "adct_compress_psnr_dense": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _vp, _vp]),
     "adct_transform_matrix": (_i32, [_i32, _vp]),
+    "adct_diag_energy": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp]),
+    "adct_sweep_psnr": (_i32, [_vp, _i64, _i64, _vp, _i32, _vp, _vp, _vp]),
     "adct_status_string": (ctypes.c_char_p, [_i32]),
     "adct_last_cuda_error": (_i32, []),
     "adct_version": (_i32, []),
@@ -137,6 +139,30 @@ def compress_psnr_dense(x, r: int, transform: str = "dct", matrix=None, sse=None
                                            cm.ctypes.data if cm is not None else None, sse.data_ptr(),
                                            _stream(stream)), "adct_compress_psnr_dense")
     return sse
+
+
+def diag_energy(x, energy=None, stream=None):
+    """adct_diag_energy: exact per-image anti-diagonal energies sum W Y^2 (uint64 [n, 16], device)."""
+    torch = _torch()
+    p, n, h, w, pitch, istr = _plane(x, 1)
+    if energy is None:
+        energy = torch.empty((n, 16), dtype=torch.int64, device=x.device)
+    _check(load().adct_diag_energy(p, n, h, w, pitch, istr, energy.data_ptr(), _stream(stream)),
+           "adct_diag_energy")
+    return energy
+
+
+def sweep_psnr(energy, pixels: int, r_list, stream=None):
+    """adct_sweep_psnr: (sse, psnr) [len(r_list), n] for triangular r from diag_energy's output."""
+    torch = _torch()
+    n = energy.shape[0]
+    nr = len(r_list)
+    sse = torch.empty((nr, n), dtype=torch.float64, device=energy.device)
+    ps = torch.empty_like(sse)
+    rl = (ctypes.c_int * nr)(*[int(v) for v in r_list])
+    _check(load().adct_sweep_psnr(energy.data_ptr(), n, pixels, rl, nr, sse.data_ptr(), ps.data_ptr(),
+                                  _stream(stream)), "adct_sweep_psnr")
+    return sse, ps
 
 
 def quant_reciprocals(q: float) -> np.ndarray:

@@ -401,6 +401,52 @@ adct_status adct_compress_psnr_dense(const uint8_t* src, int64_t n, int64_t h, i
   return launch_tma_kernel(k_compress_dense<0>, map, p, p.tiles, s);
 }
 
+adct_status adct_diag_energy(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch, int64_t img_stride,
+                             uint64_t* energy, adct_stream_t stream) {
+  adct_status st = check_geom(n, h, w);
+  if (st) return st;
+  if (!energy) return ADCT_EINVAL;
+  if ((st = check_plane(src, h, w, pitch, img_stride))) return st;
+  if ((uintptr_t)energy & 7u) return ADCT_EALIGN;
+  CUtensorMap map;
+  if ((st = make_u8_map(&map, src, n, h, w, pitch, img_stride))) return st;
+  DiagParams p;
+  memset(&p, 0, sizeof(p));
+  p.geo = make_geo(h, w);
+  p.tiles = p.geo.per_img * n;
+  p.h = (int)h;
+  p.w = (int)w;
+  p.energy = reinterpret_cast<unsigned long long*>(energy);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(energy, 0, sizeof(uint64_t) * 16 * (size_t)n, s);
+  if (e != cudaSuccess) return cuda_fail(e);
+  return launch_tma_kernel(k_diag_energy<0>, map, p, p.tiles, s);
+}
+
+adct_status adct_sweep_psnr(const uint64_t* energy, int64_t n, int64_t pixels, const int* r_list, int n_r, double* sse,
+                            double* psnr, adct_stream_t stream) {
+  if (!energy || !r_list || !sse || !psnr || n < 1 || pixels < 1 || n_r < 1 || n_r > 16) return ADCT_EINVAL;
+  if (((uintptr_t)energy & 7u) || ((uintptr_t)sse & 7u) || ((uintptr_t)psnr & 7u)) return ADCT_EALIGN;
+  SweepList L;
+  memset(&L, 0, sizeof(L));
+  L.n_r = n_r;
+  for (int k = 0; k < n_r; ++k) {
+    int s = -1;
+    for (int d = 0; d < 15; ++d) {  // r = number of positions with k + l <= d
+      const int rd = d <= 7 ? (d + 1) * (d + 2) / 2 : 64 - (14 - d) * (15 - d) / 2;
+      if (rd == r_list[k]) s = d;
+    }
+    if (s < 0) return ADCT_EINVAL;  // only full anti-diagonal r: 1,3,6,10,15,21,28,36,43,49,54,58,61,63,64
+    L.diag[k] = s;
+  }
+  const int64_t total = n * n_r;
+  k_sweep_psnr<0><<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const unsigned long long*>(energy), n, L, (double)pixels, sse, psnr);
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
+}
+
 adct_status adct_quant_reciprocals(float q, float* c_out) {
   if (!c_out || !(q > 0.f) || isinf(q)) return ADCT_EINVAL;
   for (int k = 0; k < 8; ++k)

@@ -449,6 +449,86 @@ __global__ void __launch_bounds__(WARPS * 32, 3)
   if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v);
 }
 
+// ------------------------------------------------------------------------------------------
+// Parseval sweep: one read of the images gives the SSE of EVERY triangular r.
+// C = D C0 is orthogonal, so the zonal reconstruction error of a block equals the energy
+// of its discarded orthonormal coefficients: 576^2 SSE = 576 * sum_{zz >= r} W Y^2 with
+// W = 576 / (d_i d_j).  The kernel accumulates, per image, the exact integer energy
+// E_s = sum_blocks sum_{k+l=s} W_kl Y_kl^2 of each anti-diagonal s = 0..14 (u64); for a
+// triangular r = (s+1)(s+2)/2 the SSE is sum_{s' > s} E_s' / 576.  No inverse is computed, so this
+// is NOT the fwd+zonal+inv path of the headline metric and is reported separately.
+// ------------------------------------------------------------------------------------------
+struct DiagParams {
+  TileGeo geo;
+  int64_t tiles;
+  int cshift;
+  int h, w;
+  unsigned long long* energy;  // [n][16]
+};
+
+template <int UNUSED = 0>
+__global__ void __launch_bounds__(WARPS * 32, 4)
+    k_diag_energy(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ DiagParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ring = smem + warp * (STAGES * TILE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * STAGES * TILE_BYTES) + warp * STAGES;
+  const WarpSched ws{(int64_t)blockIdx.x * WARPS + warp, (int64_t)gridDim.x * WARPS, p.tiles, p.cshift};
+  int cur = -1;
+  long long E[15];
+#pragma unroll
+  for (int s = 0; s < 15; ++s) E[s] = 0;
+  auto flush = [&](int img) {
+#pragma unroll
+    for (int s = 0; s < 15; ++s) {
+      long long v = E[s];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && img >= 0) atomicAdd(p.energy + (int64_t)img * 16 + s, (unsigned long long)v);
+      E[s] = 0;
+    }
+  };
+  tma_ring_loop<STAGES>(&tmap, ws, p.geo, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
+    if (img != cur) {
+      flush(cur);
+      cur = img;
+    }
+    uint32_t P[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      pack_rows(lds64(tile + i * TILE_W + lane * 8), lds64(tile + (i + 8) * TILE_W + lane * 8), P[i]);
+    uint32_t Y[8][8];
+    fwd2d<0x8000u, 64>(P, Y);  // lo lane biased by 2^15, hi lane exact
+    static_for<64>([&](auto KLc) {
+      constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
+      constexpr int W = wval(k, l);
+      const int a = (int)(Y[k][l] & 0xFFFFu) - 32768;   // Y of block A
+      const int b = (int)Y[k][l] >> 16;                 // Y of block B
+      E[k + l] += (long long)a * (W * a) + (long long)b * (W * b);  // IMAD + IMAD.WIDE each, exact
+    });
+  });
+  flush(cur);
+}
+
+// SSE / PSNR of triangular r from the anti-diagonal energies: SSE(r_s) = sum_{s' > s} E_s' / 576.
+struct SweepList {
+  int n_r;
+  int diag[16];  // anti-diagonal index s of each requested triangular r
+};
+template <int UNUSED = 0>
+__global__ void k_sweep_psnr(const unsigned long long* __restrict__ energy, int64_t n, const __grid_constant__ SweepList L,
+                             double pixels, double* __restrict__ sse, double* __restrict__ psnr) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * L.n_r) return;
+  const int64_t img = i % n;
+  const int k = (int)(i / n);
+  unsigned long long acc = 0;
+  for (int s = L.diag[k] + 1; s < 15; ++s) acc += energy[img * 16 + s];
+  const double e = (double)acc / 576.0;
+  sse[i] = e;
+  psnr[i] = (acc == 0) ? __longlong_as_double(0x7ff0000000000000ll) : 10.0 * log10(65025.0 * pixels / e);
+}
+
 typedef void (*CompressKernel)(CUtensorMap, CompressParams);
 // zonal kernels k_compress<r, ZONAL, RECON_NONE>, instantiated in zonal_part*.cu (4 TUs)
 CompressKernel zonal_kernel(int r);

@@ -21,7 +21,7 @@ def header_functions():
 def test_library_exports_every_declared_symbol():
     lib = A.load()
     names = header_functions()
-    assert len(names) == 12
+    assert len(names) == 14
     for name in names:
         assert hasattr(lib, name), name
         assert name in _lib.SIGNATURES, name
@@ -132,3 +132,13 @@ def test_dense_validation():
     assert lib.adct_compress_psnr_dense(16, 1, 8, 16, 16, 128, 0, 1, None, 64, None) == E     # r = 0
     assert lib.adct_compress_psnr_dense(16, 1, 8, 16, 16, 128, 10, 4, None, 64, None) == E    # custom w/o matrix
     assert lib.adct_compress_psnr_dense(16, 1, 8, 16, 16, 128, 10, 9, None, 64, None) == E    # bad enum
+
+
+def test_sweep_validation():
+    lib = A.load()
+    E = _lib.ADCT_EINVAL
+    rl = (ctypes.c_int * 2)(1, 4)      # r = 4 does not end on a full anti-diagonal
+    assert lib.adct_sweep_psnr(16, 1, 64, rl, 2, 32, 48, None) == E
+    rl = (ctypes.c_int * 1)(10)
+    assert lib.adct_sweep_psnr(16, 0, 64, rl, 1, 32, 48, None) == E
+    assert lib.adct_diag_energy(16, 1, 8, 16, 16, 128, 0, None) == E

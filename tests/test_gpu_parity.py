@@ -376,3 +376,42 @@ def test_c2_dct_curve_vs_oracle():
     for r in (1, 2, 5, 10, 16, 30, 45, 63):
         p_dct = O.mean_psnr(host(A.compress_psnr_dense(x, r, "dct")), px)
         assert abs(p_dct - O.mean_psnr(O.compress_zonal_sse(imgs, r, O.dct_matrix()), px)) <= PSNR_TOL
+
+
+# ------------------------------------------------------------------ Parseval sweep (F3)
+
+def oracle_diag_energy(imgs):
+    d = np.array([8, 6, 4, 6, 8, 6, 4, 6])
+    W = 576 // np.outer(d, d)
+    Y = O.to_blocks(O.forward_int(imgs)).astype(np.int64)          # [n, H, W, 8, 8]
+    E = (W * Y * Y).sum(axis=(1, 2))                                 # [n, 8, 8]
+    ii, jj = np.indices((8, 8))
+    return np.stack([E[:, ii + jj == s].sum(axis=1) for s in range(15)], axis=1)
+
+
+def test_diag_energy_bit_exact_and_sweep_sse():
+    imgs = np.concatenate([S.corpus_c2(4, 64, 96), impulse_images().reshape(1, 128 * 8, 8)[:, :64, :]
+                           .repeat(12, axis=2)[:, :, :96],
+                           np.full((1, 64, 96), 255, dtype=np.uint8)])
+    x = dev(imgs)
+    E = host(A.diag_energy(x))
+    want = oracle_diag_energy(imgs)
+    assert np.array_equal(E[:, :15].astype(np.int64), want)
+    rs = [1, 3, 6, 10, 15, 21, 28, 36, 43, 49, 54, 58, 61, 63, 64]
+    sse, ps = A.sweep_psnr(A.diag_energy(x), 64 * 96, rs)
+    sse = host(sse)
+    for k, r in enumerate(rs):
+        exact = O.compress_zonal_sse(imgs, r)
+        assert np.allclose(sse[k], exact, rtol=1e-10, atol=1e-6), r
+        fused = host(A.compress_psnr(x, r))
+        if r < 64:
+            check_sse(fused, sse[k], 64 * 96)
+        else:
+            assert np.all(sse[k] == 0) and np.all(fused < 1e-6)
+
+
+def test_diag_energy_c5_full_size_sampled():
+    x = S.device_mixed(64, 4096, 4096, seed=1)
+    E = host(A.diag_energy(x))
+    sample = [0, 1, 2, 63]
+    assert np.array_equal(E[sample, :15].astype(np.int64), oracle_diag_energy(host(x[sample])))
