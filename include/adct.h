@@ -156,7 +156,20 @@ typedef enum {
 
 adct_status adct_compress_psnr_dense(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
                                      int64_t img_stride, int r, adct_transform_t t, const double* custom,
-                                     double* sse, adct_stream_t stream);
+                                     float* recon /* nullable f32 plane */, int64_t recon_pitch,
+                                     int64_t recon_img_stride, double* sse, adct_stream_t stream);
+
+/*
+ * adct_uqi — universal quality index: per image, the mean over all
+ * 8x8 sliding windows (stride 1) of Q = 4 s_xy mx my / ((s_x^2 + s_y^2)(mx^2 + my^2)) between
+ * the uint8 original x and an f32 reconstruction y (e.g. ADCT_RECON_F32 of adct_compress_psnr
+ * or the dense path's recon).  Q = L S, L = 2 mx my / (mx^2 + my^2), S = 2 s_xy / (s_x^2 + s_y^2);
+ * reading R16: a 0/0 factor (denominator <= 1e-12 pixel^2) is 1.  x sums exact (int), y in fp64.
+ *   x   [n][h][x_pitch] uint8;  y  [n][h][y_pitch bytes] float (4-byte aligned);
+ *   uqi device double[n], overwritten.  n <= 65535.
+ */
+adct_status adct_uqi(const uint8_t* x, int64_t n, int64_t h, int64_t w, int64_t x_pitch, int64_t x_img_stride,
+                     const float* y, int64_t y_pitch, int64_t y_img_stride, double* uqi, adct_stream_t stream);
 
 /*
  * Parseval sweep: one read of the images yields the SSE of every triangular r.

@@ -32,7 +32,7 @@ __all__ = [
     "zigzag_order", "zigzag_index", "zonal_mask", "to_blocks", "from_blocks",
     "forward_int", "forward_scaled", "inverse", "reconstruct_zonal", "reconstruct_zonal_exact",
     "quantize_exact", "reconstruct_quant", "sse_per_image", "psnr", "mean_psnr",
-    "compress_zonal_sse", "compress_quant_sse", "round_u8",
+    "compress_zonal_sse", "compress_quant_sse", "round_u8", "uqi", "ape",
 ]
 
 
@@ -326,3 +326,46 @@ def compress_quant_sse(img: np.ndarray, q: float) -> np.ndarray:
     if img.ndim == 2:
         img = img[None]
     return sse_per_image(img, reconstruct_quant(img, q))
+
+
+# --------------------------------------------------------------------------------------
+# Universal quality index and APE (second workload)
+# --------------------------------------------------------------------------------------
+
+def uqi(a: np.ndarray, b: np.ndarray, window: int = 8) -> float:
+    """Mean over all window x window sliding windows (stride 1) of the Wang-Bovik index
+    Q = 4 s_xy mx my / ((s_x^2 + s_y^2)(mx^2 + my^2))  (sample moments; the 1/N vs 1/(N-1)
+    normalisation cancels), i.e. Q = L * S with L = 2 mx my / (mx^2 + my^2) (luminance) and
+    S = 2 s_xy / (s_x^2 + s_y^2) (correlation x contrast).  Reading R16 for degenerate windows:
+    a 0/0 factor is 1 — L = 1 when mx^2 + my^2 <= 1e-12, S = 1 when s_x^2 + s_y^2 <= 1e-12
+    (pixel^2 units; a non-flat or non-black 8-bit window is far above these: s_x^2 >= 63/64^2,
+    mx^2 >= 1/64^2, so the guards only absorb floating-point round-off of the reconstruction).
+    float64, moments about the window mean."""
+    x = np.asarray(a, dtype=np.float64)
+    y = np.asarray(b, dtype=np.float64)
+    if x.shape != y.shape or x.ndim != 2:
+        raise ValueError("uqi: two images of equal 2-D shape")
+    if x.shape[0] < window or x.shape[1] < window:
+        raise ValueError("uqi: image smaller than the window")
+    from numpy.lib.stride_tricks import sliding_window_view as swv
+    X = swv(x, (window, window))
+    Y = swv(y, (window, window))
+    mx = X.mean(axis=(2, 3))
+    my = Y.mean(axis=(2, 3))
+    dx = X - mx[..., None, None]
+    dy = Y - my[..., None, None]
+    vx = (dx * dx).mean(axis=(2, 3))
+    vy = (dy * dy).mean(axis=(2, 3))
+    cxy = (dx * dy).mean(axis=(2, 3))
+    d1 = vx + vy
+    d2 = mx * mx + my * my
+    L = np.where(d2 <= 1e-12, 1.0, 2 * mx * my / np.where(d2 <= 1e-12, 1.0, d2))
+    S_ = np.where(d1 <= 1e-12, 1.0, 2 * cxy / np.where(d1 <= 1e-12, 1.0, d1))
+    return float((L * S_).mean())
+
+
+def ape(value: float, reference: float) -> float:
+    """Absolute percentage error relative to the exact-DCT value: 100 |v - ref| / |ref|."""
+    if reference == 0:
+        raise ValueError("ape: zero reference")
+    return 100.0 * abs(value - reference) / abs(reference)

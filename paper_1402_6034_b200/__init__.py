@@ -6,8 +6,8 @@ forward, inverse, compress_psnr, psnr, compress_psnr_host.  See DESIGN.md.
 from ._lib import (AdctError, compress_psnr, compress_psnr_dense, compress_psnr_host, diag_energy,  # noqa: F401
                    empty_plane, sweep_psnr,
                    forward, inverse, launch_count, load, psnr, quant_reciprocals, to_device,
-                   transform_matrix, version)
+                   transform_matrix, uqi, version)
 
 __all__ = ["forward", "inverse", "compress_psnr", "psnr", "compress_psnr_host", "load", "launch_count",
            "version", "AdctError", "empty_plane", "to_device", "quant_reciprocals",
-           "compress_psnr_dense", "transform_matrix", "diag_energy", "sweep_psnr"]
+           "compress_psnr_dense", "transform_matrix", "diag_energy", "sweep_psnr", "uqi"]

@@ -29,7 +29,9 @@ SIGNATURES = {
     "adct_compress_psnr_host": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _i32, _f32, _vp, _i64,
                                        _vp, _vp, _vp]),
     "adct_quant_reciprocals": (_i32, [_f32, _vp]),
-    "adct_compress_psnr_dense": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _vp, _vp]),
+    "adct_compress_psnr_dense": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _vp, _i64, _i64,
+                                        _vp, _vp]),
+    "adct_uqi": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp]),
     "adct_transform_matrix": (_i32, [_i32, _vp]),
     "adct_diag_energy": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp]),
     "adct_sweep_psnr": (_i32, [_vp, _i64, _i64, _vp, _i32, _vp, _vp, _vp]),
@@ -126,8 +128,11 @@ def transform_matrix(kind: str) -> np.ndarray:
     return out.reshape(8, 8)
 
 
-def compress_psnr_dense(x, r: int, transform: str = "dct", matrix=None, sse=None, stream=None):
-    """adct_compress_psnr_dense: the block pipeline with a dense fp64 8x8 transform (comparators)."""
+def compress_psnr_dense(x, r: int, transform: str = "dct", matrix=None, sse=None, recon: bool = False,
+                        recon_out=None, stream=None):
+    """adct_compress_psnr_dense: the block pipeline with a dense 8x8 transform (comparators).
+
+    Returns sse (float64 [n]) or (sse, recon f32 [n, h, w]) when recon=True."""
     torch = _torch()
     p, n, h, w, pitch, istr = _plane(x, 1)
     if sse is None:
@@ -135,10 +140,28 @@ def compress_psnr_dense(x, r: int, transform: str = "dct", matrix=None, sse=None
     cm = None
     if transform == "custom":
         cm = np.ascontiguousarray(np.asarray(matrix, dtype=np.float64).reshape(64))
+    rp, rpitch, ristr = None, 0, 0
+    if recon:
+        if recon_out is None:
+            recon_out = empty_plane(n, h, w, torch.float32, x.device)
+        rp, _n, _h, _w, rpitch, ristr = _plane(recon_out, 4)
     _check(load().adct_compress_psnr_dense(p, n, h, w, pitch, istr, r, TRANSFORMS[transform],
-                                           cm.ctypes.data if cm is not None else None, sse.data_ptr(),
-                                           _stream(stream)), "adct_compress_psnr_dense")
-    return sse
+                                           cm.ctypes.data if cm is not None else None, rp, rpitch, ristr,
+                                           sse.data_ptr(), _stream(stream)), "adct_compress_psnr_dense")
+    return (sse, recon_out) if recon else sse
+
+
+def uqi(x, y, out=None, stream=None):
+    """adct_uqi: per-image mean UQI (8x8 sliding windows) between uint8 x and f32 y (device)."""
+    torch = _torch()
+    p, n, h, w, pitch, istr = _plane(x, 1)
+    q, n2, h2, w2, ypitch, yistr = _plane(y, 4)
+    if (n, h, w) != (n2, h2, w2):
+        raise ValueError("uqi: x and y shapes differ")
+    if out is None:
+        out = torch.empty((n,), dtype=torch.float64, device=x.device)
+    _check(load().adct_uqi(p, n, h, w, pitch, istr, q, ypitch, yistr, out.data_ptr(), _stream(stream)), "adct_uqi")
+    return out
 
 
 def diag_energy(x, energy=None, stream=None):

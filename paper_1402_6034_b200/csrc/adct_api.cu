@@ -366,12 +366,14 @@ adct_status adct_transform_matrix(adct_transform_t t, double* out) {
 
 adct_status adct_compress_psnr_dense(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
                                      int64_t img_stride, int r, adct_transform_t t, const double* custom,
+                                     float* recon, int64_t recon_pitch, int64_t recon_img_stride,
                                      double* sse, adct_stream_t stream) {
   adct_status st = check_geom(n, h, w);
   if (st) return st;
   if (r < 1 || r > 64 || !sse) return ADCT_EINVAL;
   if (t < ADCT_T_PROPOSED || t > ADCT_T_CUSTOM || (t == ADCT_T_CUSTOM && !custom)) return ADCT_EINVAL;
   if ((st = check_plane(src, h, w, pitch, img_stride))) return st;
+  if (recon && (st = check_plane(recon, h, w * 4, recon_pitch, recon_img_stride))) return st;
   if ((uintptr_t)sse & 7u) return ADCT_EALIGN;
   CUtensorMap map;
   if ((st = make_u8_map(&map, src, n, h, w, pitch, img_stride))) return st;
@@ -382,6 +384,9 @@ adct_status adct_compress_psnr_dense(const uint8_t* src, int64_t n, int64_t h, i
   p.h = (int)h;
   p.w = (int)w;
   p.sse = sse;
+  p.recon = recon;
+  p.recon_pitch = recon_pitch;
+  p.recon_img_stride = recon_img_stride;
   for (int k = 0; k < 8; ++k)
     for (int l = 0; l < 8; ++l)
       if (zz_host(k, l) < r) p.keep_raster |= 1ull << (k * 8 + l);
@@ -444,6 +449,37 @@ adct_status adct_sweep_psnr(const uint64_t* energy, int64_t n, int64_t pixels, c
       reinterpret_cast<const unsigned long long*>(energy), n, L, (double)pixels, sse, psnr);
   ++g_launches;
   cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
+}
+
+adct_status adct_uqi(const uint8_t* x, int64_t n, int64_t h, int64_t w, int64_t x_pitch, int64_t x_img_stride,
+                     const float* y, int64_t y_pitch, int64_t y_img_stride, double* uqi, adct_stream_t stream) {
+  adct_status st = check_geom(n, h, w);
+  if (st) return st;
+  if (!x || !y || !uqi) return ADCT_EINVAL;
+  if (x_pitch < w || x_img_stride < h * x_pitch || y_pitch < 4 * w || y_img_stride < h * y_pitch) return ADCT_EINVAL;
+  if (((uintptr_t)y & 3u) || (y_pitch & 3) || (y_img_stride & 3) || ((uintptr_t)uqi & 7u)) return ADCT_EALIGN;
+  if (n > 65535) return ADCT_EINVAL;
+  UqiParams p;
+  memset(&p, 0, sizeof(p));
+  p.x = x;
+  p.x_pitch = x_pitch;
+  p.x_img_stride = x_img_stride;
+  p.y = y;
+  p.y_pitch = y_pitch;
+  p.y_img_stride = y_img_stride;
+  p.h = (int)h;
+  p.w = (int)w;
+  p.tiles_x = (int)((w - 7 + UQI_T - 1) / UQI_T);
+  p.tiles_y = (int)((h - 7 + UQI_T - 1) / UQI_T);
+  p.inv_windows = 1.0 / ((double)(h - 7) * (double)(w - 7));
+  p.out = uqi;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(uqi, 0, sizeof(double) * (size_t)n, s);
+  if (e != cudaSuccess) return cuda_fail(e);
+  k_uqi<0><<<dim3(p.tiles_x, p.tiles_y, (unsigned)n), 256, 0, s>>>(p);
+  ++g_launches;
+  e = cudaGetLastError();
   return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
 }
 

@@ -368,6 +368,8 @@ struct DenseParams {
   int cshift;
   int h, w;
   double* sse;
+  float* recon;  // optional f32 reconstruction plane
+  int64_t recon_pitch, recon_img_stride;
   uint64_t keep_raster;  // bit k*8+l: coefficient (k, l) kept
   float T[64];           // row-major T[m][n]
 };
@@ -376,7 +378,8 @@ __device__ __forceinline__ float px_byte(uint2 wv, int j) {
   return (float)((j < 4 ? (wv.x >> (8 * j)) : (wv.y >> (8 * (j - 4)))) & 0xFFu);
 }
 
-__device__ __forceinline__ double dense_block_sse(const uint8_t* tile, int lane, int b, const DenseParams& p) {
+__device__ __forceinline__ double dense_block_sse(const uint8_t* tile, int lane, int b, const DenseParams& p,
+                                                  int img, int ty, int tx) {
   float Xh[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
@@ -408,6 +411,18 @@ __device__ __forceinline__ double dense_block_sse(const uint8_t* tile, int lane,
       for (int k = 0; k < 8; ++k) wi = fmaf(p.T[k * 8 + i], z[k], wi);
 #pragma unroll
       for (int n = 0; n < 8; ++n) Xh[i][n] = fmaf(wi, p.T[l * 8 + n], Xh[i][n]);
+    }
+  }
+  if (p.recon) {
+    const int col = tx * TILE_W + lane * 8, row0 = ty * TILE_H + b * 8;
+    if (col < p.w && row0 < p.h) {
+      uint8_t* base = reinterpret_cast<uint8_t*>(p.recon) + (int64_t)img * p.recon_img_stride + (int64_t)col * 4;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4* q = reinterpret_cast<float4*>(base + (int64_t)(row0 + i) * p.recon_pitch);
+        q[0] = make_float4(Xh[i][0], Xh[i][1], Xh[i][2], Xh[i][3]);
+        q[1] = make_float4(Xh[i][4], Xh[i][5], Xh[i][6], Xh[i][7]);
+      }
     }
   }
   double acc = 0.0;
@@ -442,8 +457,8 @@ __global__ void __launch_bounds__(WARPS * 32, 3)
       cur = img;
       acc = 0.0;
     }
-    acc += dense_block_sse(tile, lane, 0, p);
-    acc += dense_block_sse(tile, lane, 1, p);
+    acc += dense_block_sse(tile, lane, 0, p, img, ty, tx);
+    acc += dense_block_sse(tile, lane, 1, p, img, ty, tx);
   });
   const double v = warp_sum(acc);
   if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v);
@@ -527,6 +542,100 @@ __global__ void k_sweep_psnr(const unsigned long long* __restrict__ energy, int6
   const double e = (double)acc / 576.0;
   sse[i] = e;
   psnr[i] = (acc == 0) ? __longlong_as_double(0x7ff0000000000000ll) : 10.0 * log10(65025.0 * pixels / e);
+}
+
+// ------------------------------------------------------------------------------------------
+// Universal quality index: mean over all 8x8 sliding windows
+// (stride 1) of Q = 4 C Mx My / ((Vx + Vy)(Mx^2 + My^2)) with C = N Sxy - Sx Sy,
+// V = N S.. - S.^2, M = S. (window sums, N = 64; the normalisations cancel) = L * S with
+// L = 2 Mx My / (Mx^2 + My^2), S = 2 C / (Vx + Vy); reading R16: a 0/0 factor is 1.
+// x sums are exact integers, y sums fp64.  One CTA (256 threads) per 32x32 block of window
+// origins: the 39x39 x / y patch is staged in shared memory, horizontal 8-sums per row, then
+// vertical 8-sums per window.
+// ------------------------------------------------------------------------------------------
+constexpr int UQI_T = 32, UQI_P = UQI_T + 7;
+struct UqiParams {
+  const uint8_t* x;
+  int64_t x_pitch, x_img_stride;
+  const float* y;
+  int64_t y_pitch, y_img_stride;
+  int h, w, tiles_x, tiles_y;
+  double inv_windows;  // 1 / ((h - 7)(w - 7))
+  double* out;         // [n]
+};
+
+template <int UNUSED = 0>
+__global__ void __launch_bounds__(256) k_uqi(const __grid_constant__ UqiParams p) {
+  __shared__ int hx[UQI_P][UQI_T], hxx[UQI_P][UQI_T];
+  __shared__ double hy[UQI_P][UQI_T], hyy[UQI_P][UQI_T], hxy[UQI_P][UQI_T];
+  __shared__ uint8_t px[UQI_P][UQI_P + 1];
+  __shared__ float py[UQI_P][UQI_P + 1];
+  __shared__ double red[8];
+  const int img = blockIdx.z, ty = blockIdx.y, tx = blockIdx.x;
+  const int r0 = ty * UQI_T, c0 = tx * UQI_T;
+  const uint8_t* xb = p.x + (int64_t)img * p.x_img_stride;
+  const uint8_t* yb = reinterpret_cast<const uint8_t*>(p.y) + (int64_t)img * p.y_img_stride;
+  for (int i = threadIdx.x; i < UQI_P * UQI_P; i += blockDim.x) {
+    const int r = i / UQI_P, c = i % UQI_P, gr = r0 + r, gc = c0 + c;
+    const bool ok = gr < p.h && gc < p.w;
+    px[r][c] = ok ? xb[(int64_t)gr * p.x_pitch + gc] : 0;
+    py[r][c] = ok ? *reinterpret_cast<const float*>(yb + (int64_t)gr * p.y_pitch + (int64_t)gc * 4) : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < UQI_P * UQI_T; i += blockDim.x) {
+    const int r = i / UQI_T, c = i % UQI_T;
+    int sx = 0, sxx = 0;
+    double sy = 0, syy = 0, sxy = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int a = px[r][c + k];
+      const double b = (double)py[r][c + k];
+      sx += a;
+      sxx += a * a;
+      sy += b;
+      syy = fma(b, b, syy);
+      sxy = fma((double)a, b, sxy);
+    }
+    hx[r][c] = sx;
+    hxx[r][c] = sxx;
+    hy[r][c] = sy;
+    hyy[r][c] = syy;
+    hxy[r][c] = sxy;
+  }
+  __syncthreads();
+  double q_acc = 0.0;
+  for (int i = threadIdx.x; i < UQI_T * UQI_T; i += blockDim.x) {
+    const int r = i / UQI_T, c = i % UQI_T;
+    if (r0 + r > p.h - 8 || c0 + c > p.w - 8) continue;  // window must fit in the image
+    long long Sx = 0, Sxx = 0;
+    double Sy = 0, Syy = 0, Sxy = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      Sx += hx[r + k][c];
+      Sxx += hxx[r + k][c];
+      Sy += hy[r + k][c];
+      Syy += hyy[r + k][c];
+      Sxy += hxy[r + k][c];
+    }
+    const double Mx = (double)Sx, My = Sy;
+    const double Vx = (double)(64 * Sxx - Sx * Sx);                // exact integer
+    const double Vy = fmax(fma(64.0, Syy, -Sy * Sy), 0.0);
+    const double C = fma(64.0, Sxy, -Mx * My);
+    const double d1 = Vx + Vy, d2 = fma(Mx, Mx, My * My);
+    // Q = L * S, a 0/0 factor taken as 1 (reading R16); guards 1e-12 pixel^2 = 4096e-12 in sum units
+    const double L = (d2 <= 4.096e-9) ? 1.0 : 2.0 * Mx * My / d2;
+    const double Sc = (d1 <= 4.096e-9) ? 1.0 : 2.0 * C / d1;
+    const double q = L * Sc;
+    q_acc += q;
+  }
+  q_acc = warp_sum(q_acc);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = q_acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int k = 0; k < 8; ++k) t += red[k];
+    atomicAdd(p.out + img, t * p.inv_windows);
+  }
 }
 
 typedef void (*CompressKernel)(CUtensorMap, CompressParams);

@@ -21,7 +21,7 @@ def header_functions():
 def test_library_exports_every_declared_symbol():
     lib = A.load()
     names = header_functions()
-    assert len(names) == 14
+    assert len(names) == 15
     for name in names:
         assert hasattr(lib, name), name
         assert name in _lib.SIGNATURES, name
@@ -129,9 +129,10 @@ def test_library_matrices_match_oracle():
 def test_dense_validation():
     lib = A.load()
     E = _lib.ADCT_EINVAL
-    assert lib.adct_compress_psnr_dense(16, 1, 8, 16, 16, 128, 0, 1, None, 64, None) == E     # r = 0
-    assert lib.adct_compress_psnr_dense(16, 1, 8, 16, 16, 128, 10, 4, None, 64, None) == E    # custom w/o matrix
-    assert lib.adct_compress_psnr_dense(16, 1, 8, 16, 16, 128, 10, 9, None, 64, None) == E    # bad enum
+    assert lib.adct_compress_psnr_dense(16, 1, 8, 16, 16, 128, 0, 1, None, None, 0, 0, 64, None) == E   # r = 0
+    assert lib.adct_compress_psnr_dense(16, 1, 8, 16, 16, 128, 10, 4, None, None, 0, 0, 64, None) == E  # custom, no T
+    assert lib.adct_compress_psnr_dense(16, 1, 8, 16, 16, 128, 10, 9, None, None, 0, 0, 64, None) == E  # bad enum
+    assert lib.adct_uqi(16, 1, 8, 16, 16, 128, 0, 64, 512, 64, None) == E                               # y NULL
 
 
 def test_sweep_validation():

@@ -415,3 +415,44 @@ def test_diag_energy_c5_full_size_sampled():
     E = host(A.diag_energy(x))
     sample = [0, 1, 2, 63]
     assert np.array_equal(E[sample, :15].astype(np.int64), oracle_diag_energy(host(x[sample])))
+
+
+# ------------------------------------------------------------------ UQI / APE (F2)
+
+def test_uqi_kernel_vs_oracle():
+    imgs = np.concatenate([S.corpus_c2(3, 64, 96), rng.integers(0, 256, (1, 64, 96), dtype=np.uint8),
+                           np.full((1, 64, 96), 77, dtype=np.uint8)])
+    x = dev(imgs)
+    for r in (1, 6, 21, 64):
+        _sse, rec = A.compress_psnr(x, r, recon="f32")
+        got = host(A.uqi(x, rec))
+        recn = host(rec).astype(np.float64)
+        want = np.array([O.uqi(imgs[i], recn[i]) for i in range(len(imgs))])
+        assert np.abs(got - want).max() <= 1e-9, (r, got, want)
+    # identical images -> 1; inverted -> negative
+    f = torch.from_numpy(imgs.astype(np.float32)).cuda()
+    yf = A.empty_plane(*imgs.shape, dtype=torch.float32)
+    yf.copy_(f)
+    assert np.allclose(host(A.uqi(x, yf)), 1.0, atol=1e-12)
+    yf.copy_(255.0 - f)
+    inv = host(A.uqi(x, yf))
+    assert np.all(inv[[0, 1, 3]] < 0)      # textured images: anticorrelated windows
+    assert abs(inv[4] - 2 * 77 * 178 / (77 ** 2 + 178 ** 2)) < 1e-12   # flat image: luminance term
+
+
+def test_uqi_ape_proposed_vs_dct_end_to_end():
+    """APE of the average UQI and MSE relative to the exact DCT (Figs. 4-5's quantities)
+    on a small C2-like corpus: GPU pipeline vs the oracle pipeline."""
+    imgs = S.corpus_c2(6, 128, 128)
+    x = dev(imgs)
+    for r in (3, 10, 28):
+        sp, rp = A.compress_psnr(x, r, recon="f32")
+        sd, rd = A.compress_psnr_dense(x, r, "dct", recon=True)
+        uq_p, uq_d = host(A.uqi(x, rp)).mean(), host(A.uqi(x, rd)).mean()
+        o_p = np.mean([O.uqi(im, O.reconstruct_zonal(im[None], r)[0]) for im in imgs])
+        o_d = np.mean([O.uqi(im, O.reconstruct_zonal(im[None], r, O.dct_matrix())[0]) for im in imgs])
+        assert abs(O.ape(uq_p, uq_d) - O.ape(o_p, o_d)) <= 1e-3
+        mse_p, mse_d = host(sp).mean() / 128 ** 2, host(sd).mean() / 128 ** 2
+        om_p = O.compress_zonal_sse(imgs, r).mean() / 128 ** 2
+        om_d = O.compress_zonal_sse(imgs, r, O.dct_matrix()).mean() / 128 ** 2
+        assert abs(O.ape(mse_p, mse_d) - O.ape(om_p, om_d)) <= 1e-2

@@ -339,3 +339,50 @@ def test_synth_generators_shapes_and_ranges():
     assert c.shape == (6, 64, 64)
     assert len({c[i].tobytes() for i in range(6)}) == 6
     assert 20 < a.std() < 80
+
+
+# ---------------------------------------------------------------- UQI / APE (F2, reading R16)
+
+def brute_uqi(a, b, wdw=8):
+    """Python-loop UQI with (N-1)-normalised moments, as in the Wang-Bovik definition."""
+    h, w = a.shape
+    tot, cnt = 0.0, 0
+    for i in range(h - wdw + 1):
+        for j in range(w - wdw + 1):
+            xs = [float(v) for v in a[i:i + wdw, j:j + wdw].ravel()]
+            ys = [float(v) for v in b[i:i + wdw, j:j + wdw].ravel()]
+            N = len(xs)
+            mx, my = sum(xs) / N, sum(ys) / N
+            vx = sum((v - mx) ** 2 for v in xs) / (N - 1)
+            vy = sum((v - my) ** 2 for v in ys) / (N - 1)
+            c = sum((p - mx) * (q - my) for p, q in zip(xs, ys)) / (N - 1)
+            d1, d2 = vx + vy, mx * mx + my * my
+            lum = 1.0 if d2 <= 1e-12 else 2 * mx * my / d2
+            ctr = 1.0 if d1 <= 1e-12 * (N / (N - 1)) else 2 * c / d1
+            q_ = lum * ctr
+            tot += q_
+            cnt += 1
+    return tot / cnt
+
+
+def test_uqi_brute_force_and_properties():
+    a = rng.integers(0, 256, size=(16, 16)).astype(float)
+    b = np.clip(a + rng.normal(0, 20, size=a.shape), 0, 255)
+    assert abs(O.uqi(a, b) - brute_uqi(a, b)) < 1e-12          # 1/N vs 1/(N-1) cancels
+    assert abs(O.uqi(a, b) - O.uqi(b, a)) < 1e-15              # symmetric
+    assert abs(O.uqi(3.5 * a, 3.5 * b) - O.uqi(a, b)) < 1e-12   # common-scale invariant
+    assert abs(O.uqi(a, a) - 1.0) < 1e-12                      # identical non-constant -> 1
+    inv = 255 - a
+    assert O.uqi(a, inv) < 0                                   # anticorrelated windows
+    c = np.full((12, 12), 7.0)
+    assert O.uqi(c, c) == 1.0                                  # R16: both constant, equal
+    assert abs(O.uqi(c, 2 * c) - 2 * 7 * 14 / (49 + 196)) < 1e-15
+    z = np.zeros((9, 9))
+    assert O.uqi(z, z) == 1.0
+    osc = np.tile([[-5.0, 5.0], [5.0, -5.0]], (6, 6))          # zero mean, non-flat vs a black window
+    assert O.uqi(np.zeros((12, 12)), osc) == 0.0
+    assert abs(O.uqi(c, c + 1e-9 * rng.normal(size=c.shape)) - 1.0) < 1e-9   # round-off on a flat region
+    with pytest.raises(ValueError):
+        O.uqi(np.zeros((4, 4)), np.zeros((4, 4)))
+    assert O.ape(1.1, 1.0) == pytest.approx(10.0)
+    assert O.ape(2.0, 2.0) == 0.0

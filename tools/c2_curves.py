@@ -1,7 +1,8 @@
-"""C2 curves on the GPU (BASELINE configs[1]): mean PSNR per r = 1..64 over the 45 synthetic
-512x512 images for the proposed transform (fused fast path), the exact DCT and the SDCT (dense
-comparator path), plus MSE absolute percentage error vs the exact DCT (Fig. 5's quantity).
-Writes CSV (transform,r,avg_mse,avg_psnr,ape_mse) to stdout or --out."""
+"""C2 curves on the GPU (BASELINE configs[1]): per r = 1..64 over the 45 synthetic 512x512
+images, for the proposed transform (fused fast path), the exact DCT and the SDCT (dense comparator
+path): average MSE, PSNR and UQI, and the absolute percentage errors of average MSE and UQI vs the
+exact DCT (the quantities of the paper's Figs. 3-5).
+Writes CSV (transform,r,avg_mse,avg_psnr,avg_uqi,ape_mse,ape_uqi) to stdout or --out."""
 import argparse
 import os
 import sys
@@ -19,17 +20,21 @@ a = ap.parse_args()
 imgs = S.corpus_c2()
 x = A.to_device(imgs)
 px = 512 * 512
-rows = ["transform,r,avg_mse,avg_psnr,ape_mse"]
+rows = ["transform,r,avg_mse,avg_psnr,avg_uqi,ape_mse,ape_uqi"]
 for r in range(1, 65):
-    res = {"proposed": A.compress_psnr(x, r), "dct": A.compress_psnr_dense(x, r, "dct"),
-           "sdct": A.compress_psnr_dense(x, r, "sdct")}
+    sp, rp = A.compress_psnr(x, r, recon="f32")
+    sd, rd = A.compress_psnr_dense(x, r, "dct", recon=True)
+    ss, rs = A.compress_psnr_dense(x, r, "sdct", recon=True)
+    res = {"proposed": (sp, A.uqi(x, rp)), "dct": (sd, A.uqi(x, rd)), "sdct": (ss, A.uqi(x, rs))}
     torch.cuda.synchronize()
-    mse = {k: v.cpu().numpy() / px for k, v in res.items()}
-    for k, m in mse.items():
+    vals = {k: (v[0].cpu().numpy() / px, v[1].cpu().numpy()) for k, v in res.items()}
+    ref_mse, ref_uqi = vals["dct"][0].mean(), vals["dct"][1].mean()
+    for k, (m, u) in vals.items():
         with np.errstate(divide="ignore"):
             psnr = np.where(m > 0, 10 * np.log10(255.0 ** 2 / np.where(m > 0, m, 1)), np.inf)
-        ape = 100 * abs(m.mean() - mse["dct"].mean()) / mse["dct"].mean() if mse["dct"].mean() > 0 else 0.0
-        rows.append(f"{k},{r},{m.mean():.6f},{np.mean(psnr):.6f},{ape:.4f}")
+        ape_m = 100 * abs(m.mean() - ref_mse) / ref_mse if ref_mse > 0 else 0.0
+        ape_u = 100 * abs(u.mean() - ref_uqi) / abs(ref_uqi)
+        rows.append(f"{k},{r},{m.mean():.6f},{np.mean(psnr):.6f},{u.mean():.8f},{ape_m:.4f},{ape_u:.5f}")
 txt = "\n".join(rows) + "\n"
 if a.out:
     open(a.out, "w").write(txt)
