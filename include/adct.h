@@ -48,7 +48,8 @@ typedef struct CUstream_st* adct_stream_t; /* = cudaStream_t */
 typedef enum {
   ADCT_OK = 0,
   ADCT_EINVAL = 1, /* n < 1, h or w not a positive multiple of 8, r outside [1,64], q < 0 or NaN,
-                      pitch < row bytes, img_stride < h * pitch, unknown enum, NULL required pointer */
+                      pitch < row bytes, img_stride < h * pitch, unknown enum, NULL required pointer,
+                      or more than 2^30 tiles of 16 x 256 pixels (4 TiB of uint8) in one call */
   ADCT_EALIGN = 2, /* a pointer not 16-byte aligned, or a pitch / image stride not a multiple of 16
                       (TMA global-address and stride rules) */
   ADCT_ECUDA = 3   /* CUDA launch or driver error; see adct_last_cuda_error() */

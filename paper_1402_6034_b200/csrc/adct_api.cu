@@ -67,6 +67,9 @@ bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 adct_status check_geom(int64_t n, int64_t h, int64_t w) {
   if (n < 1 || h < 8 || w < 8 || (h & 7) || (w & 7)) return ADCT_EINVAL;
   if (n > INT32_MAX || h > INT32_MAX || w > INT32_MAX) return ADCT_EINVAL;
+  // the device-side tile cursors are 32-bit: at most 2^30 tiles of 16 x 256 pixels per call
+  const int64_t tiles = n * ((h + TILE_H - 1) / TILE_H) * ((w + TILE_W - 1) / TILE_W);
+  if (tiles > (int64_t(1) << 30)) return ADCT_EINVAL;
   return ADCT_OK;
 }
 

@@ -178,6 +178,39 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
   return f2add(f2add(s01, s23), f2add(s45, s67));
 }
 
+// Residual form of the zonal error (compile-time r, SSE only).  C = D C0 is orthogonal, so
+// C0^T (W . Y) C0 = 576 x for every block (r = 64 is lossless, pin P8) and, by linearity,
+//     576 x - R_r = C0^T (W . (1 - M_r) . Y) C0,
+// i.e. the reconstruction error of the zonal step is the same inverse butterfly applied to the
+// coefficients the mask discards.  Every node is an integer below 2^24 (tools/exactness_bounds.py),
+// so this equals the direct form bit for bit; it needs no pixel re-read and no 576 x, and for
+// large r the discarded set is the smaller one.  Returns the lane's sum of e^2 (576 units).
+template <int R>
+__device__ __forceinline__ float2 compress_resid(const uint32_t (&Y)[8][8], const CompressParams& p) {
+  constexpr int RM = RESID + R;
+  float2 V[64];
+  static_for<64>([&](auto KLc) {
+    constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
+    if constexpr (kept(RM, k, l)) {
+      constexpr int c = wclass(k, l);
+      V[kl] = f2fma(biased_pair(Y[k][l]), f2(p.tab.wc[c]), f2(p.tab.cc[c]));  // W . (1 - M) . Y, exact
+    }
+  });
+  float2 acc[8];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) acc[n] = f2(0.f);
+  inverse2d<RM>(V, [&](auto Ic, auto row) {
+    using cuda::std::get;
+    static_for<8>([&](auto Nc) {
+      constexpr int N = decltype(Nc)::value;
+      acc[N] = sqacc(get<N>(row), acc[N]);
+    });
+  });
+  const float2 s01 = f2add(acc[0], acc[1]), s23 = f2add(acc[2], acc[3]);
+  const float2 s45 = f2add(acc[4], acc[5]), s67 = f2add(acc[6], acc[7]);
+  return f2add(f2add(s01, s23), f2add(s45, s67));
+}
+
 // ------------------------------------------------------------------------------------------
 // Fused compress kernel: every warp owns a TMA ring of ST stages and runs forward + inverse +
 // error on each tile (one warp tile = 16 rows x 256 columns = one block pair per lane).
@@ -187,13 +220,18 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
 // ------------------------------------------------------------------------------------------
 // measured on B200 (profiles/r01_tune_compress.txt): small r wants occupancy, large r registers
 constexpr int compress_stages(int R) { return 2; }
-constexpr int compress_minb(int R) { return R <= 6 ? 5 : (R <= 24 ? 4 : 3); }
-
-constexpr int compress_prefetch(int R) { return 0; }
+// residual form from this r on: cheaper once the discarded set is the smaller one
+#ifndef ADCT_RESID_FROM
+#define ADCT_RESID_FROM 24
+#endif
+constexpr int compress_resid_r(int R) { return R >= ADCT_RESID_FROM && R < 64; }
+constexpr int compress_minb(int R) {
+  return compress_resid_r(R) ? (R < 30 ? 3 : 4) : (R <= 6 ? 5 : (R <= 24 ? 4 : 3));
+}
 
 template <int R, int MODE, int RECON, int ST = compress_stages((MODE == MODE_QUANT) ? RT : R),
           int MINB = (MODE == MODE_ZONAL && RECON == REC_NONE) ? compress_minb(R) : 3,
-          int PF = compress_prefetch(R)>
+          bool RES = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT && compress_resid_r(R))>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     k_compress(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CompressParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -201,10 +239,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint8_t* ring = smem + warp * (ST * TILE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * ST * TILE_BYTES) + warp * ST;
-  const WarpSched ws{(int64_t)blockIdx.x * WARPS + warp, (int64_t)gridDim.x * WARPS, p.tiles, p.cshift};
+  const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
   int cur = -1;
   double acc = 0.0;
-  tma_ring_loop<ST, PF>(&tmap, ws, p.geo, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
+  tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
+                      [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {  // warp-uniform: flush the finished image's partial SSE
       const double v = warp_sum(acc);
       if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v * kSseScale);
@@ -212,8 +251,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
       acc = 0.0;
     }
     uint32_t Y[8][8];
-    compress_fwd<R, MODE>(tile, lane, Y);
-    const float2 e2 = compress_inv<R, MODE, RECON>(Y, tile, lane, p, img, ty, tx);
+    float2 e2;
+    if constexpr (RES) {
+      compress_fwd<RESID + R, MODE>(tile, lane, Y);
+      e2 = compress_resid<R>(Y, p);
+    } else {
+      compress_fwd<R, MODE>(tile, lane, Y);
+      e2 = compress_inv<R, MODE, RECON>(Y, tile, lane, p, img, ty, tx);
+    }
     acc += (double)e2.x + (double)e2.y;
   });
   const double v = warp_sum(acc);

@@ -1,0 +1,131 @@
+"""Exactness proof for the fp32 inverse of the fused compress kernel (R13/R17).
+
+The kernel's zonal inverse runs the transposed 22-addition graph (columns, then rows) in fp32 on
+integer-valued inputs V = W (.) Y (+ a DC bias).  Every node is then an integer, and fp32 is exact
+as long as every node's magnitude stays below 2^24.  Each node is an affine function of the 64
+pixels of a block, so its exact range over all uint8 blocks is [c + 255 sum(a-), c + 255 sum(a+)].
+This script propagates those affine forms through the same graph, in the same operation order as
+adct_device.cuh inv8 / inverse2d, for every r and both kernel variants:
+
+  direct    V = W (.) M_r (.) Y, plus DC_BIAS on V_00 (so every output is R + DC_BIAS, and the
+            error is one FMA: e = 576 (128 + x) - (R + 73728) = 576 x - R)
+  residual  V = W (.) (1 - M_r) (.) Y (the discarded coefficients): output = 576 x - R directly
+            (576 x = C0^T (W (.) Y) C0 for every block, the r = 64 case of P8)
+
+Prints the largest |node| per r and variant and exits non-zero if any reaches 2^24.
+Pure host arithmetic on T (the displayed C0); it models the kernel, not the oracle.
+"""
+from __future__ import annotations
+
+import sys
+
+import numpy as np
+
+T = np.array([[1, 1, 1, 1, 1, 1, 1, 1],
+              [1, 1, 1, 0, 0, -1, -1, -1],
+              [1, 0, 0, -1, -1, 0, 0, 1],
+              [1, 0, -1, -1, 1, 1, 0, -1],
+              [1, -1, -1, 1, 1, -1, -1, 1],
+              [1, -1, 0, 1, -1, 0, 1, -1],
+              [0, -1, 1, 0, 0, 1, -1, 0],
+              [0, -1, 1, -1, 1, -1, 1, 0]], dtype=np.int64)
+D = np.array([8, 6, 4, 6, 8, 6, 4, 6])
+W = 576 // np.outer(D, D)
+DC_BIAS = 73728  # 576 * 128
+
+
+def zz(i: int, j: int) -> int:
+    s = i + j
+    before = sum((t + 1) if t < 8 else 15 - t for t in range(s))
+    lo, hi = (0, s) if s < 8 else (s - 7, 7)
+    return before + ((i - lo) if s & 1 else (hi - i))
+
+
+class Bound:
+    def __init__(self):
+        self.max = 0
+
+    def see(self, f):
+        if f is None:
+            return f
+        a, c = f[:64], f[64]
+        lo = c + 255 * a[a < 0].sum()
+        hi = c + 255 * a[a > 0].sum()
+        self.max = max(self.max, abs(lo), abs(hi))
+        return f
+
+
+def add(B, a, b):
+    if a is None:
+        return b
+    if b is None:
+        return a
+    return B.see(a + b)
+
+
+def sub(B, a, b):
+    if b is None:
+        return a
+    if a is None:
+        return -b
+    return B.see(a - b)
+
+
+def inv8(B, x):
+    p, q = add(B, x[0], x[4]), sub(B, x[0], x[4])
+    a0, a3 = add(B, p, x[2]), sub(B, p, x[2])
+    a1, a2 = sub(B, q, x[6]), add(B, q, x[6])
+    b0 = add(B, add(B, x[1], x[3]), x[5])
+    b1 = sub(B, sub(B, x[1], x[5]), x[7])
+    b2 = add(B, sub(B, x[1], x[3]), x[7])
+    b3 = sub(B, sub(B, x[5], x[3]), x[7])
+    return [add(B, a0, b0), add(B, a1, b1), add(B, a2, b2), add(B, a3, b3),
+            sub(B, a3, b3), sub(B, a2, b2), sub(B, a1, b1), sub(B, a0, b0)]
+
+
+def forms_Y():
+    """Y_kl = sum_ij T_ki T_lj x_ij as affine forms (64 coefficients + constant)."""
+    Y = np.zeros((8, 8, 65), dtype=np.int64)
+    for k in range(8):
+        for l in range(8):
+            Y[k, l, :64] = np.outer(T[k], T[l]).reshape(64)
+    return Y
+
+
+def run(r: int, variant: str):
+    B = Bound()
+    Y = forms_Y()
+    V = [[None] * 8 for _ in range(8)]
+    for k in range(8):
+        for l in range(8):
+            kept = zz(k, l) < r
+            live = kept if variant == "direct" else not kept
+            if live:
+                V[k][l] = B.see(W[k, l] * Y[k, l])
+    if variant == "direct":
+        V[0][0] = V[0][0].copy()
+        V[0][0][64] += DC_BIAS
+        B.see(V[0][0])
+    U = [inv8(B, [V[k][l] for k in range(8)]) for l in range(8)]
+    out = [inv8(B, [U[l][i] for l in range(8)]) for i in range(8)]
+    # check the final identity: direct -> R + bias, residual -> 576 x - R
+    return B.max, out
+
+
+def main():
+    worst = 0
+    for variant in ("direct", "residual"):
+        row = []
+        for r in range(1, 65):
+            if variant == "residual" and r == 64:
+                continue
+            m, _ = run(r, variant)
+            worst = max(worst, m)
+            row.append(f"{r}:{m}")
+        print(variant, " ".join(row))
+    print("max |node| =", worst, "< 2^24 =", 1 << 24, "->", "EXACT" if worst < (1 << 24) else "NOT EXACT")
+    return 0 if worst < (1 << 24) else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

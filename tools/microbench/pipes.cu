@@ -59,6 +59,43 @@ __global__ void __launch_bounds__(256) kern(uint32_t* out, uint32_t seed, unsign
         asm volatile("prmt.b32 %0, %0, %1, 0x5140;" : "+r"(f[c]) : "r"(r[(c + 2) % CH]));
         asm volatile("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(rr[(c + 4) % CH]) : "l"(rr[(c + 5) % CH]), "l"(rr[(c + 6) % CH]));
       }
+      // conversions: byte -> f32 (I2F.U8 with byte select), int -> f32 (I2FP), f16 -> f32 (HADD2.F32)
+      if (OP == 19) asm volatile("{.reg .u32 t; shr.u32 t, %0, 8; cvt.rn.f32.u8 %0, t;}" : "+r"(r[c]));
+      if (OP == 20) asm volatile("cvt.rn.f32.u32 %0, %0;" : "+r"(r[c]));
+      if (OP == 21) asm volatile("{.reg .f16 h; mov.b32 {h, _}, %0; cvt.f32.f16 %0, h;}" : "+r"(r[c]));
+      if (OP == 22) {  // PRMT + I2F.U8 interleaved: separate pipes?
+        asm volatile("prmt.b32 %0, %0, %1, 0x5140;" : "+r"(r[c]) : "r"(k1));
+        asm volatile("cvt.rn.f32.u8 %0, %0;" : "+r"(f[c]));
+      }
+      if (OP == 23) {  // FFMA2 + I2F.U8 interleaved
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %0;" : "+l"(rr[c]) : "l"(kk));
+        asm volatile("cvt.rn.f32.u8 %0, %0;" : "+r"(f[c]));
+      }
+      if (OP == 24) {  // PRMT + HADD2.F32 interleaved
+        asm volatile("prmt.b32 %0, %0, %1, 0x5140;" : "+r"(r[c]) : "r"(k1));
+        asm volatile("{.reg .f16 h; mov.b32 {h, _}, %0; cvt.f32.f16 %0, h;}" : "+r"(f[c]));
+      }
+      if (OP == 25) {  // FFMA2 + HADD2.F32 interleaved
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %0;" : "+l"(rr[c]) : "l"(kk));
+        asm volatile("{.reg .f16 h; mov.b32 {h, _}, %0; cvt.f32.f16 %0, h;}" : "+r"(f[c]));
+      }
+      if (OP == 26) {  // PRMT + I2FP.F32.U32 interleaved
+        asm volatile("prmt.b32 %0, %0, %1, 0x5140;" : "+r"(r[c]) : "r"(k1));
+        asm volatile("cvt.rn.f32.u32 %0, %0;" : "+r"(f[c]));
+      }
+      if (OP == 27) {  // FFMA2 + I2FP.F32.U32 interleaved
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %0;" : "+l"(rr[c]) : "l"(kk));
+        asm volatile("cvt.rn.f32.u32 %0, %0;" : "+r"(f[c]));
+      }
+      if (OP == 28) asm volatile("dp4a.u32.u32 %0, %0, %1, %0;" : "+r"(r[c]) : "r"(k1));
+      if (OP == 29) {  // PRMT + IMAD interleaved (IMAD on the FMA pipe?)
+        asm volatile("prmt.b32 %0, %0, %1, 0x5140;" : "+r"(r[c]) : "r"(k1));
+        asm volatile("mad.lo.s32 %0, %0, %1, %2;" : "+r"(f[c]) : "r"(k1), "r"(k2));
+      }
+      if (OP == 30) {  // FFMA2 + IMAD interleaved
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %0;" : "+l"(rr[c]) : "l"(kk));
+        asm volatile("mad.lo.s32 %0, %0, %1, %2;" : "+r"(f[c]) : "r"(k1), "r"(k2));
+      }
     }
   }
   unsigned long long t1 = clock64();
@@ -122,5 +159,17 @@ int main() {
   run<16>("fadd2 live", 2, 1, sms);
   run<17>("prmt live", 1, 1, sms);
   run<18>("mix4 live", 1, 4, sms);
+  run<19>("i2f.u8(+shf)", 1, 2, sms);
+  run<20>("i2fp.u32", 1, 1, sms);
+  run<21>("hadd2.f32", 1, 1, sms);
+  run<22>("prmt+i2f.u8", 1, 2, sms);
+  run<23>("ffma2+i2f.u8", 1, 2, sms);
+  run<24>("prmt+hadd2.f32", 1, 2, sms);
+  run<25>("ffma2+hadd2.f32", 1, 2, sms);
+  run<26>("prmt+i2fp", 1, 2, sms);
+  run<27>("ffma2+i2fp", 1, 2, sms);
+  run<28>("dp4a", 1, 1, sms);
+  run<29>("prmt+imad", 1, 2, sms);
+  run<30>("ffma2+imad", 1, 2, sms);
   return 0;
 }

@@ -18,9 +18,10 @@ static double* g_sse;
 static int g_sms;
 static const int N = 256, H = 4096, W = 4096;
 
-template <int R, int ST, int MINB, int PF = 0>
+static double g_ref[4096];
+template <int R, int ST, int MINB, int PF = 0, bool RES = false>  // PF: unused (kept for the sweep table)
 void run(int cshift_max = 4) {
-  auto k = k_compress<R, MODE_ZONAL, REC_NONE, ST, MINB, PF>;
+  auto k = k_compress<R, MODE_ZONAL, REC_NONE, ST, MINB, RES>;
   CompressParams p;
   memset(&p, 0, sizeof(p));
   p.geo.tiles_x = W / TILE_W;
@@ -45,7 +46,13 @@ void run(int cshift_max = 4) {
   int cshift = cshift_max;
   while (cshift > 0 && (p.tiles >> cshift) < 2LL * grid * WARPS) --cshift;
   p.cshift = cshift;
+  cudaMemset(g_sse, 0, N * sizeof(double));
   k<<<grid, WARPS * 32, smem>>>(g_map, p);
+  double hs[N];
+  cudaMemcpy(hs, g_sse, N * sizeof(double), cudaMemcpyDeviceToHost);
+  double maxrel = 0;
+  if (!RES) memcpy(g_ref, hs, sizeof(hs));
+  for (int i = 0; i < N; ++i) maxrel = fmax(maxrel, fabs(hs[i] - g_ref[i]) / fmax(g_ref[i], 1e-300));
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
@@ -57,16 +64,31 @@ void run(int cshift_max = 4) {
   cudaEventElapsedTime(&ms, a, b);
   ms /= 5;
   double gbs = (double)N * H * W / ms / 1e6;
-  printf("r=%2d ST=%d MINB=%d PF=%d occ=%d cshift=%d: %.3f ms %6.0f GB/s frac %.3f %s\n", R, ST, MINB, PF, occ, cshift, ms, gbs,
+  printf("r=%2d %s ST=%d MINB=%d PF=%d occ=%d cshift=%d: %.3f ms %6.0f GB/s frac %.3f sse_vs_direct %.2e %s\n", R,
+         RES ? "resid " : "direct", ST, MINB, PF, occ, cshift, ms, gbs, maxrel,
          gbs / 6534.1, cudaGetErrorString(cudaGetLastError()));
   fflush(stdout);
 }
 
 template <int R, int MB>
 void sweep() {
-  run<R, 2, MB, 0>();
-  run<R, 3, MB - 1, 0>();
+  run<R, 2, MB, 0, false>();
+  run<R, 2, 3, 0, true>();
+  run<R, 2, 4, 0, true>();
+  run<R, 2, 5, 0, true>();
 }
+template <int R>
+void sweep_occ() {
+  run<R, 2, 5, 0, false>();
+  run<R, 2, 6, 0, false>();
+  run<R, 2, 7, 0, false>();
+  run<R, 3, 5, 0, false>();
+  run<R, 3, 6, 0, false>();
+}
+#ifndef SWEEPS
+#define SWEEPS sweep<1, 5>(); sweep<3, 5>(); sweep<6, 5>(); sweep<10, 4>(); sweep<15, 4>(); sweep<21, 4>(); \
+  sweep<28, 3>(); sweep<36, 3>();
+#endif
 
 int main() {
   cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, 0);
@@ -87,17 +109,15 @@ int main() {
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
   cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+#ifdef TUNE_L2
+  // L2-resident control: images overlap (stride 64 KB), footprint ~32 MB < 126 MB L2
+  cuuint64_t str[2] = {(cuuint64_t)W, (cuuint64_t)W * 16};
+#else
   cuuint64_t str[2] = {(cuuint64_t)W, (cuuint64_t)W * H};
+#endif
   cuuint32_t box[3] = {TILE_W, TILE_H, 1}, es[3] = {1, 1, 1};
   ((EncFn)fp)(&g_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, g_src, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  sweep<1, 5>();
-  sweep<3, 5>();
-  sweep<6, 5>();
-  sweep<10, 4>();
-  sweep<15, 4>();
-  sweep<21, 4>();
-  sweep<28, 3>();
-  sweep<36, 3>();
+  SWEEPS
   return 0;
 }
