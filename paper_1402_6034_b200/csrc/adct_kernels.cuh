@@ -11,6 +11,8 @@
 
 #include "adct_device.cuh"
 
+#include <cuda_fp16.h>
+
 #include <cuda/std/array>
 
 namespace adct {
@@ -124,10 +126,27 @@ __device__ __forceinline__ void compress_fwd(const uint8_t* tile, int lane, uint
 
 // Inverse half: zonal weights / quantiser, inverse with C^T, error against the staged pixels.
 // Returns this lane's partial sum of squared errors (576 units for ZONAL) as an fp32 pair.
-template <int R, int MODE, int RECON>
+// F16 (compile-time r, zonal, SSE only): the first F16 output rows take their pixels through the
+// f16 magic (one PRMT makes 1024 + x for two pixels, HADD2.F32 widens each on the FMA pipe) and
+// the error in one FFMA2: e = R' - 576 (1024 + x) with R' = R + 589824 injected at the DC weight
+// (T's first row is all ones, so a constant added to V_00 shifts every output by the same
+// amount; |R'| < 2^24 stays exact, tools/exactness_bounds.py).  The other rows keep the f32 magic
+// (two PRMTs per pixel pair on the ALU pipe).  Same instruction count, different ALU/FMA split.
+constexpr float DC_BIAS16 = 589824.0f;  // 576 * 1024
+__device__ __forceinline__ float2 px16(uint32_t wa, uint32_t wb, int pair, int hi) {
+  const uint32_t ha = __byte_perm(wa, 0x64646464u, pair ? 0x4342 : 0x4140);
+  const uint32_t hb = __byte_perm(wb, 0x64646464u, pair ? 0x4342 : 0x4140);
+  const __half2 a = *reinterpret_cast<const __half2*>(&ha), b = *reinterpret_cast<const __half2*>(&hb);
+  return hi ? make_float2(__high2float(a), __high2float(b)) : make_float2(__low2float(a), __low2float(b));
+}
+__device__ __forceinline__ float2 err16(float2 F, FV<false> r) { return f2fma(F, f2(-576.f), r.v); }
+__device__ __forceinline__ float2 err16(float2 F, FV<true> r) { return f2fma(F, f2(576.f), r.v); }
+
+template <int R, int MODE, int RECON, int F16 = 0>
 __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const uint8_t* tile, int lane,
                                                const CompressParams& p, int img, int ty, int tx) {
   constexpr int RF = (MODE == MODE_QUANT) ? RT : R;
+  static_assert(F16 == 0 || (MODE == MODE_ZONAL && RECON == REC_NONE && RF < RT), "f16 error route: zonal SSE only");
   float2 V[64];
   static_for<64>([&](auto KLc) {
     constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
@@ -136,7 +155,8 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
         // scalar weight / offset broadcast to both lanes from 12 loop-invariant class constants:
         // an FFMA2 that reads three distinct register pairs issues at 1/3 rate on B200
         constexpr int c = wclass(k, l);
-        V[kl] = f2fma(biased_pair(Y[k][l]), f2(p.tab.wc[c]), f2(p.tab.cc[c]));  // W . M . Y, exact
+        const float cc = (F16 > 0 && kl == 0) ? p.tab.cc[c] + DC_BIAS16 : p.tab.cc[c];
+        V[kl] = f2fma(biased_pair(Y[k][l]), f2(p.tab.wc[c]), f2(cc));  // W . M . Y (+ bias), exact
       } else if constexpr (MODE == MODE_ZONAL) {
         V[kl] = f2fma(biased_pair(Y[k][l]), f2(p.tab.w[kl].x), f2(p.tab.c[kl].x));  // runtime mask in w
       } else {
@@ -163,12 +183,18 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
     float2 xr[8];
     static_for<8>([&](auto Nc) {
       constexpr int N = decltype(Nc)::value;
-      // ZONAL: 576 x - R, exact integers; QUANT: x - x^ (fp32, irrational weights)
-      const float2 y = (MODE == MODE_ZONAL) ? px576(N < 4 ? wa.x : wa.y, N < 4 ? wb.x : wb.y, N & 3)
-                                            : px1(N < 4 ? wa.x : wa.y, N < 4 ? wb.x : wb.y, N & 3);
-      const float2 e = rsub(y, get<N>(row));
-      acc[N] = f2fma(e, e, acc[N]);
-      if constexpr (RECON != REC_NONE) xr[N] = val(get<N>(row));
+      if constexpr (I < F16) {
+        const float2 F = px16(N < 4 ? wa.x : wa.y, N < 4 ? wb.x : wb.y, (N >> 1) & 1, N & 1);
+        const float2 e = err16(F, get<N>(row));  // R' - 576 (1024 + x) = R - 576 x, exact
+        acc[N] = f2fma(e, e, acc[N]);
+      } else {
+        // ZONAL: 576 x - R, exact integers; QUANT: x - x^ (fp32, irrational weights)
+        const float2 y = (MODE == MODE_ZONAL) ? px576b<(F16 > 0)>(N < 4 ? wa.x : wa.y, N < 4 ? wb.x : wb.y, N & 3)
+                                              : px1(N < 4 ? wa.x : wa.y, N < 4 ? wb.x : wb.y, N & 3);
+        const float2 e = rsub(y, get<N>(row));
+        acc[N] = f2fma(e, e, acc[N]);
+        if constexpr (RECON != REC_NONE) xr[N] = val(get<N>(row));
+      }
     });
     if constexpr (RECON != REC_NONE)
       store_recon_row<RECON, (MODE == MODE_ZONAL)>(rbase, p.recon_pitch, p.h, p.w, ty * TILE_H + I, col, xr);
@@ -225,13 +251,18 @@ constexpr int compress_stages(int R) { return 2; }
 #define ADCT_RESID_FROM 24
 #endif
 constexpr int compress_resid_r(int R) { return R >= ADCT_RESID_FROM && R < 64; }
+// output rows per tile that take the f16 error route (ALU -> FMA pipe rebalancing, compress_inv)
+// measured on B200 (profiles/r01_tune_f16_rows.txt): only the ALU-bound small r gain (+1-2 %)
+constexpr int compress_f16_rows(int R) { return R == 1 ? 8 : (R <= 3 ? 4 : 0); }
+// measured on B200 (profiles/r01_tune_minb.txt): small r wants occupancy, mid r registers
 constexpr int compress_minb(int R) {
-  return compress_resid_r(R) ? (R < 30 ? 3 : 4) : (R <= 6 ? 5 : (R <= 24 ? 4 : 3));
+  return compress_resid_r(R) ? 4 : (R == 1 ? 6 : (R <= 3 ? 5 : (R <= 10 ? 4 : 3)));
 }
 
 template <int R, int MODE, int RECON, int ST = compress_stages((MODE == MODE_QUANT) ? RT : R),
           int MINB = (MODE == MODE_ZONAL && RECON == REC_NONE) ? compress_minb(R) : 3,
-          bool RES = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT && compress_resid_r(R))>
+          bool RES = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT && compress_resid_r(R)),
+          int F16 = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_f16_rows(R) : 0>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     k_compress(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CompressParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -257,7 +288,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
       e2 = compress_resid<R>(Y, p);
     } else {
       compress_fwd<R, MODE>(tile, lane, Y);
-      e2 = compress_inv<R, MODE, RECON>(Y, tile, lane, p, img, ty, tx);
+      e2 = compress_inv<R, MODE, RECON, F16>(Y, tile, lane, p, img, ty, tx);
     }
     acc += (double)e2.x + (double)e2.y;
   });

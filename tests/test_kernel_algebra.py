@@ -1,0 +1,75 @@
+"""Host-side proofs for the arithmetic the fused compress kernel relies on (no GPU).
+
+tools/exactness_bounds.py models the kernel's fp32 inverse (the transposed 22-addition graph, columns
+then rows, in the kernel's operation order) on affine forms of the 64 pixels of a block.  Here the
+model's outputs are compared, as exact integer forms, with plain matrix algebra written out in the
+test, for every r:
+
+* direct   (kernel rows that compute e = 576 x - R):  graph output == T^T (W . M_r . Y) T  (+ DC bias)
+* residual (kernel for r >= ADCT_RESID_FROM):          graph output == 576 x - T^T (W . M_r . Y) T,
+  i.e. C0^T (W . (1 - M_r) . Y) C0 = 576 x - R, which rests on r = 64 being lossless (pin P8)
+
+and every intermediate node stays below 2^24 in magnitude, so fp32 evaluates it exactly.
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+import exactness_bounds as EB  # noqa: E402
+
+
+def _affine_R(r):
+    """R = T^T (W . M_r . Y) T with Y = T X T^T, as a (64 outputs) x (64 pixels) integer matrix."""
+    T, W = EB.T, EB.W
+    M = np.array([[EB.zz(i, j) < r for j in range(8)] for i in range(8)])
+    G = np.zeros((64, 64), dtype=np.int64)
+    for p in range(64):  # impulse response of pixel p
+        X = np.zeros((8, 8), dtype=np.int64)
+        X[p // 8, p % 8] = 1
+        Y = T @ X @ T.T
+        G[:, p] = (T.T @ (W * M * Y) @ T).reshape(64)
+    return G
+
+
+def _forms(out):
+    """graph outputs out[i][n] (affine forms) -> (64 x 64 coefficient matrix, 64 constants)"""
+    A = np.zeros((64, 64), dtype=np.int64)
+    c = np.zeros(64, dtype=np.int64)
+    for i in range(8):
+        for n in range(8):
+            f = out[i][n]
+            if f is not None:
+                A[i * 8 + n] = f[:64]
+                c[i * 8 + n] = f[64]
+    return A, c
+
+
+@pytest.mark.parametrize("r", list(range(1, 65)))
+def test_direct_graph_is_R(r):
+    for bias in EB.DC_BIASES:
+        m, out = EB.run(r, "direct", bias)
+        A, c = _forms(out)
+        assert np.array_equal(A, _affine_R(r))
+        assert np.all(c == bias)
+        assert m < 2 ** 24
+
+
+@pytest.mark.parametrize("r", list(range(1, 64)))
+def test_residual_graph_is_error(r):
+    m, out = EB.run(r, "residual")
+    A, c = _forms(out)
+    assert np.array_equal(A, 576 * np.eye(64, dtype=np.int64) - _affine_R(r))
+    assert np.all(c == 0)
+    assert m < 2 ** 24
+
+
+def test_r64_lossless_identity():
+    # the identity the residual form rests on: T^T (W . Y) T = 576 X for every block (P8)
+    assert np.array_equal(_affine_R(64), 576 * np.eye(64, dtype=np.int64))
+
+
+def test_exactness_tool_exit_code():
+    assert EB.main() == 0

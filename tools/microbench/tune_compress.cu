@@ -19,9 +19,9 @@ static int g_sms;
 static const int N = 256, H = 4096, W = 4096;
 
 static double g_ref[4096];
-template <int R, int ST, int MINB, int PF = 0, bool RES = false>  // PF: unused (kept for the sweep table)
+template <int R, int ST, int MINB, int PF = 0, bool RES = false, int F16 = 0>  // PF: unused (kept for the sweep table)
 void run(int cshift_max = 4) {
-  auto k = k_compress<R, MODE_ZONAL, REC_NONE, ST, MINB, RES>;
+  auto k = k_compress<R, MODE_ZONAL, REC_NONE, ST, MINB, RES, F16>;
   CompressParams p;
   memset(&p, 0, sizeof(p));
   p.geo.tiles_x = W / TILE_W;
@@ -51,7 +51,7 @@ void run(int cshift_max = 4) {
   double hs[N];
   cudaMemcpy(hs, g_sse, N * sizeof(double), cudaMemcpyDeviceToHost);
   double maxrel = 0;
-  if (!RES) memcpy(g_ref, hs, sizeof(hs));
+  if (!RES && F16 == 0) memcpy(g_ref, hs, sizeof(hs));
   for (int i = 0; i < N; ++i) maxrel = fmax(maxrel, fabs(hs[i] - g_ref[i]) / fmax(g_ref[i], 1e-300));
   cudaEvent_t a, b;
   cudaEventCreate(&a);
@@ -64,9 +64,9 @@ void run(int cshift_max = 4) {
   cudaEventElapsedTime(&ms, a, b);
   ms /= 5;
   double gbs = (double)N * H * W / ms / 1e6;
-  printf("r=%2d %s ST=%d MINB=%d PF=%d occ=%d cshift=%d: %.3f ms %6.0f GB/s frac %.3f sse_vs_direct %.2e %s\n", R,
-         RES ? "resid " : "direct", ST, MINB, PF, occ, cshift, ms, gbs, maxrel,
-         gbs / 6534.1, cudaGetErrorString(cudaGetLastError()));
+  printf("r=%2d F16=%d %s ST=%d MINB=%d PF=%d occ=%d cshift=%d: %.3f ms %6.0f GB/s frac %.3f sse_vs_direct %.2e %s\n", R,
+         F16, RES ? "resid " : "direct", ST, MINB, PF, occ, cshift, ms, gbs, gbs / 6534.1,
+         maxrel, cudaGetErrorString(cudaGetLastError()));
   fflush(stdout);
 }
 
