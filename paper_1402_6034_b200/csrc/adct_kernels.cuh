@@ -253,10 +253,10 @@ constexpr int compress_stages(int R) { return 2; }
 constexpr int compress_resid_r(int R) { return R >= ADCT_RESID_FROM && R < 64; }
 // output rows per tile that take the f16 error route (ALU -> FMA pipe rebalancing, compress_inv)
 // measured on B200 (profiles/r01_tune_f16_rows.txt): only the ALU-bound small r gain (+1-2 %)
-constexpr int compress_f16_rows(int R) { return R == 1 ? 8 : (R <= 3 ? 4 : 0); }
+constexpr int compress_f16_rows(int R) { return R <= 3 ? 8 : 0; }
 // measured on B200 (profiles/r01_tune_minb.txt): small r wants occupancy, mid r registers
 constexpr int compress_minb(int R) {
-  return compress_resid_r(R) ? 4 : (R == 1 ? 6 : (R <= 3 ? 5 : (R <= 10 ? 4 : 3)));
+  return compress_resid_r(R) ? 4 : (R == 1 ? 6 : (R <= 3 ? 5 : (R <= 6 ? 4 : 3)));
 }
 
 template <int R, int MODE, int RECON, int ST = compress_stages((MODE == MODE_QUANT) ? RT : R),
@@ -267,7 +267,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     k_compress(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CompressParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   constexpr double kSseScale = (MODE == MODE_ZONAL) ? 1.0 / 331776.0 : 1.0;  // errors in 576 units (ZONAL)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: provably warp-uniform, so ptxas keeps the tile cursor in uniform
+  // registers for the TMA (no per-lane R2UR loop)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   uint8_t* ring = smem + warp * (ST * TILE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * ST * TILE_BYTES) + warp * ST;
   const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
@@ -357,11 +359,11 @@ template <int OUT>
 __global__ void __launch_bounds__(WARPS * 32, 3)
     k_forward(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ForwardParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   uint8_t* ring = smem + warp * (STAGES * TILE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * STAGES * TILE_BYTES) + warp * STAGES;
-  const WarpSched ws{(int64_t)blockIdx.x * WARPS + warp, (int64_t)gridDim.x * WARPS, p.tiles, p.cshift};
-  tma_ring_loop(&tmap, ws, p.geo, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
+  const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
+  tma_ring_loop_u<STAGES>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
     tile_forward<OUT>(tile, lane, p, img, ty, tx);
   });
 }
@@ -520,13 +522,13 @@ template <int UNUSED = 0>
 __global__ void __launch_bounds__(WARPS * 32, 3)
     k_compress_dense(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ DenseParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   uint8_t* ring = smem + warp * (STAGES * TILE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * STAGES * TILE_BYTES) + warp * STAGES;
-  const WarpSched ws{(int64_t)blockIdx.x * WARPS + warp, (int64_t)gridDim.x * WARPS, p.tiles, p.cshift};
+  const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
   int cur = -1;
   double acc = 0.0;
-  tma_ring_loop<STAGES>(&tmap, ws, p.geo, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
+  tma_ring_loop_u<STAGES>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {
       const double v = warp_sum(acc);
       if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v);
@@ -561,10 +563,10 @@ template <int UNUSED = 0>
 __global__ void __launch_bounds__(WARPS * 32, 4)
     k_diag_energy(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ DiagParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   uint8_t* ring = smem + warp * (STAGES * TILE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * STAGES * TILE_BYTES) + warp * STAGES;
-  const WarpSched ws{(int64_t)blockIdx.x * WARPS + warp, (int64_t)gridDim.x * WARPS, p.tiles, p.cshift};
+  const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
   int cur = -1;
   long long E[15];
 #pragma unroll
@@ -579,7 +581,7 @@ __global__ void __launch_bounds__(WARPS * 32, 4)
       E[s] = 0;
     }
   };
-  tma_ring_loop<STAGES>(&tmap, ws, p.geo, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
+  tma_ring_loop_u<STAGES>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {
       flush(cur);
       cur = img;
