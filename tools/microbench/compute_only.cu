@@ -18,8 +18,13 @@ __global__ void __launch_bounds__(128, MIN_CTAS) k_body(const uint8_t* src, Comp
   for (int it = 0; it < iters; ++it) {
     uint32_t Y[8][8];
     const uint8_t* t = tile[(warp + it) & 3];
-    compress_fwd<R, MODE_ZONAL>(t, lane, Y);
-    acc = f2add(acc, compress_inv<R, MODE_ZONAL, REC_NONE>(Y, t, lane, p, 0, 0, 0));
+    if constexpr (compress_resid_r(R)) {  // same per-r variant as k_compress
+      compress_fwd<RESID + R, MODE_ZONAL>(t, lane, Y);
+      acc = f2add(acc, compress_resid<R>(Y, p));
+    } else {
+      compress_fwd<R, MODE_ZONAL>(t, lane, Y);
+      acc = f2add(acc, compress_inv<R, MODE_ZONAL, REC_NONE, compress_f16_rows(R)>(Y, t, lane, p, 0, 0, 0));
+    }
   }
   if (acc.x == 1.2345f) out[0] = acc.y;
 }
@@ -65,12 +70,14 @@ int main() {
   uint8_t h[65536];
   for (int i = 0; i < 65536; ++i) h[i] = (uint8_t)((i * 2654435761u) >> 13);
   cudaMemcpy(src, h, 65536, cudaMemcpyHostToDevice);
-  run<1, 5>(src, out, sms);
-  run<1, 5>(src, out, sms, 30000);   // 5 CTAs (smem-limited like the real kernel)
-  run<1, 5>(src, out, sms, 60000);   // 3 CTAs
-  run<10, 4>(src, out, sms);
-  run<10, 4>(src, out, sms, 40000);
-  run<36, 3>(src, out, sms);
-  run<36, 3>(src, out, sms, 100000);
+  // at the library's per-r register cap (compress_minb), shared memory not limiting
+  run<1, compress_minb(1)>(src, out, sms);
+  run<3, compress_minb(3)>(src, out, sms);
+  run<6, compress_minb(6)>(src, out, sms);
+  run<10, compress_minb(10)>(src, out, sms);
+  run<15, compress_minb(15)>(src, out, sms);
+  run<21, compress_minb(21)>(src, out, sms);
+  run<28, compress_minb(28)>(src, out, sms);
+  run<36, compress_minb(36)>(src, out, sms);
   return 0;
 }
