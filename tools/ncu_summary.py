@@ -1,10 +1,20 @@
 """Summarise an ncu --set full report of k_compress launches: per-tile instruction mix, pipe
 utilisation, stall reasons and the share of stall samples inside / outside the tile body.
-Usage: python tools/ncu_summary.py report.ncu-rep [tiles_per_launch]"""
+Usage: python tools/ncu_summary.py report.ncu-rep [tiles_per_launch] [--traffic-json out.json]
+(--traffic-json writes the DRAM bytes per pixel of every k_compress / k_forward launch, the file
+bench.py reads for roofline.traffic)."""
 import csv, collections, subprocess, sys
 
-rep = sys.argv[1]
-tiles = float(sys.argv[2]) if len(sys.argv) > 2 else 32 * 4096 * 4096 / 4096
+import json
+
+args = [a for a in sys.argv[1:]]
+tj = None
+if "--traffic-json" in args:
+    i = args.index("--traffic-json")
+    tj = args[i + 1]
+    del args[i:i + 2]
+rep = args[0]
+tiles = float(args[1]) if len(args) > 1 else 32 * 4096 * 4096 / 4096
 
 
 def run(*a):
@@ -27,6 +37,21 @@ for d in data:
     st.sort(key=lambda x: -x[1])
     print("  stalls:", ", ".join(f"{h.replace('smsp__pcsamp_warps_issue_stalled_', '')} {v / tot:.3f}" for h, v in st[:9]))
 
+if tj:
+    px = tiles * 4096
+    per = {}
+    for d in data:
+        name = d[hdr.index("Kernel Name")]
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        rd = float(d[hdr.index("dram__bytes_read.sum")]) * scale[raw[1][hdr.index("dram__bytes_read.sum")]]
+        wr = float(d[hdr.index("dram__bytes_write.sum")]) * scale[raw[1][hdr.index("dram__bytes_write.sum")]]
+        per[name] = {"dram_bytes_per_px": (rd + wr) / px, "read_per_px": rd / px, "write_per_px": wr / px}
+    comp = [v["dram_bytes_per_px"] for k, v in per.items() if "k_compress" in k]
+    with open(tj, "w") as f:
+        json.dump({"source": f"ncu --set full, {int(tiles)} tiles of 4 KiB per launch "
+                             f"(summary: profiles/r01_ncu_full_summary_session3.txt)",
+                   "dram_bytes_per_px": sum(comp) / max(1, len(comp)), "per_kernel": per}, f, indent=1)
+
 src = run("--page", "source", "--csv", "--print-source", "sass").split("\n")
 blocks, cur = [], None
 for l in src:
@@ -35,7 +60,11 @@ for l in src:
         blocks.append(cur)
     elif cur is not None:
         cur.append(l)
+seen = set()
 for b in blocks:
+    if b[0] in seen:  # the source page lists each kernel once per view
+        continue
+    seen.add(b[0])
     rows = list(csv.reader(b[1:]))
     h, rs = rows[0], [r for r in rows[1:] if len(rows[0]) == len(r)]
     iE, iS, iSm = h.index("Instructions Executed"), h.index("Source"), h.index("# Samples")
