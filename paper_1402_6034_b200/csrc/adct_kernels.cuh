@@ -142,7 +142,7 @@ __device__ __forceinline__ float2 px16(uint32_t wa, uint32_t wb, int pair, int h
 __device__ __forceinline__ float2 err16(float2 F, FV<false> r) { return f2fma(F, f2(-576.f), r.v); }
 __device__ __forceinline__ float2 err16(float2 F, FV<true> r) { return f2fma(F, f2(576.f), r.v); }
 
-template <int R, int MODE, int RECON, int F16 = 0>
+template <int R, int MODE, int RECON, int F16 = 0, bool GROUPED = false>
 __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const uint8_t* tile, int lane,
                                                const CompressParams& p, int img, int ty, int tx) {
   constexpr int RF = (MODE == MODE_QUANT) ? RT : R;
@@ -175,7 +175,7 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
   const int col = tx * TILE_W + lane * 8;
   uint8_t* rbase = nullptr;
   if constexpr (RECON != REC_NONE) rbase = p.recon + (int64_t)img * p.recon_img_stride;
-  inverse2d<RF>(V, [&](auto Ic, auto row) {
+  auto err_row = [&](auto Ic, auto row) {
     constexpr int I = decltype(Ic)::value;
     using cuda::std::get;
     const uint2 wa = lds64_reload(tile + I * TILE_W + lane * 8);
@@ -198,7 +198,9 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
     });
     if constexpr (RECON != REC_NONE)
       store_recon_row<RECON, (MODE == MODE_ZONAL)>(rbase, p.recon_pitch, p.h, p.w, ty * TILE_H + I, col, xr);
-  });
+  };
+  if constexpr (GROUPED) inverse2d_grouped<RF>(V, err_row);
+  else inverse2d<RF>(V, err_row);
   const float2 s01 = f2add(acc[0], acc[1]), s23 = f2add(acc[2], acc[3]);
   const float2 s45 = f2add(acc[4], acc[5]), s67 = f2add(acc[6], acc[7]);
   return f2add(f2add(s01, s23), f2add(s45, s67));
@@ -211,7 +213,7 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
 // coefficients the mask discards.  Every node is an integer below 2^24 (tools/exactness_bounds.py),
 // so this equals the direct form bit for bit; it needs no pixel re-read and no 576 x, and for
 // large r the discarded set is the smaller one.  Returns the lane's sum of e^2 (576 units).
-template <int R>
+template <int R, bool GROUPED = false>
 __device__ __forceinline__ float2 compress_resid(const uint32_t (&Y)[8][8], const CompressParams& p) {
   constexpr int RM = RESID + R;
   float2 V[64];
@@ -225,13 +227,15 @@ __device__ __forceinline__ float2 compress_resid(const uint32_t (&Y)[8][8], cons
   float2 acc[8];
 #pragma unroll
   for (int n = 0; n < 8; ++n) acc[n] = f2(0.f);
-  inverse2d<RM>(V, [&](auto Ic, auto row) {
+  auto sq_row = [&](auto Ic, auto row) {
     using cuda::std::get;
     static_for<8>([&](auto Nc) {
       constexpr int N = decltype(Nc)::value;
       acc[N] = sqacc(get<N>(row), acc[N]);
     });
-  });
+  };
+  if constexpr (GROUPED) inverse2d_grouped<RM>(V, sq_row);
+  else inverse2d<RM>(V, sq_row);
   const float2 s01 = f2add(acc[0], acc[1]), s23 = f2add(acc[2], acc[3]);
   const float2 s45 = f2add(acc[4], acc[5]), s67 = f2add(acc[6], acc[7]);
   return f2add(f2add(s01, s23), f2add(s45, s67));
@@ -254,6 +258,11 @@ constexpr int compress_resid_r(int R) { return R >= ADCT_RESID_FROM && R < 64; }
 // output rows per tile that take the f16 error route (ALU -> FMA pipe rebalancing, compress_inv)
 // measured on B200 (profiles/r01_tune_f16_rows.txt): only the ALU-bound small r gain (+1-2 %)
 constexpr int compress_f16_rows(int R) { return R <= 3 ? 8 : 0; }
+// inverse output rows in two register-light groups (inverse2d_grouped)
+#ifndef ADCT_GROUPED
+#define ADCT_GROUPED 0
+#endif
+constexpr bool compress_grouped(int R) { return ADCT_GROUPED || (R >= 15 && R < ADCT_RESID_FROM); }
 // measured on B200 (profiles/r01_tune_minb.txt): small r wants occupancy, mid r registers
 constexpr int compress_minb(int R) {
   return compress_resid_r(R) ? 4 : (R == 1 ? 6 : (R <= 3 ? 5 : (R <= 6 ? 4 : 3)));
@@ -262,7 +271,8 @@ constexpr int compress_minb(int R) {
 template <int R, int MODE, int RECON, int ST = compress_stages((MODE == MODE_QUANT) ? RT : R),
           int MINB = (MODE == MODE_ZONAL && RECON == REC_NONE) ? compress_minb(R) : 3,
           bool RES = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT && compress_resid_r(R)),
-          int F16 = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_f16_rows(R) : 0>
+          int F16 = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_f16_rows(R) : 0,
+          bool GRP = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_grouped(R) : false>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     k_compress(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CompressParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -287,10 +297,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     float2 e2;
     if constexpr (RES) {
       compress_fwd<RESID + R, MODE>(tile, lane, Y);
-      e2 = compress_resid<R>(Y, p);
+      e2 = compress_resid<R, GRP>(Y, p);
     } else {
       compress_fwd<R, MODE>(tile, lane, Y);
-      e2 = compress_inv<R, MODE, RECON, F16>(Y, tile, lane, p, img, ty, tx);
+      e2 = compress_inv<R, MODE, RECON, F16, GRP>(Y, tile, lane, p, img, ty, tx);
     }
     acc += (double)e2.x + (double)e2.y;
   });
