@@ -126,6 +126,10 @@ adct_status adct_psnr(const double* sse, int64_t count, int64_t pixels, double* 
  * staged compactly, pitch = w rounded up to 16), runs adct_compress_psnr for each of the n_r
  * values r_list[k] (q as above) and adct_psnr, and copies PSNR back to host_psnr[k * n + i].
  *   dev_sse   device double[2 * n_r * n] scratch: SSE in [0, n_r n), PSNR in [n_r n, 2 n_r n).
+ *   When dev_buf holds at least two images and n >= 2, the images are staged in chunks of about
+ *   n / 8 through two halves of dev_buf on an internal non-blocking copy stream, so the copy of
+ *   chunk c+1 overlaps the compress passes of chunk c (event-ordered; the copy stream first waits
+ *   for work already queued on `stream`).  Otherwise copy and passes alternate on `stream`.
  *   Asynchronous: host_psnr is valid after `stream` is synchronised.
  */
 adct_status adct_compress_psnr_host(const uint8_t* host_src, int64_t n, int64_t h, int64_t w,

@@ -1,6 +1,8 @@
 // adct_api.cu — host side of the C ABI (include/adct.h): validation, TMA descriptors,
 // per-call weight / quantiser tables, dispatch and launch.
 #include "adct.h"
+
+#include <algorithm>
 #include "adct_kernels.cuh"
 
 namespace adct {
@@ -517,25 +519,70 @@ adct_status adct_compress_psnr_host(const uint8_t* host_src, int64_t n, int64_t 
   const int64_t dpitch = (w + 15) & ~(int64_t)15;
   const int64_t dimg = dpitch * h;
   if (!aligned16(dev_buf) || ((uintptr_t)dev_sse & 7u)) return ADCT_EALIGN;
-  const int64_t chunk = dev_buf_bytes / dimg;
-  if (chunk < 1) return ADCT_EINVAL;
+  const int64_t cap = dev_buf_bytes / dimg;  // images the staging buffer holds
+  if (cap < 1) return ADCT_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
-  for (int64_t i0 = 0; i0 < n; i0 += chunk) {
-    const int64_t m = (n - i0 < chunk) ? n - i0 : chunk;
-    cudaError_t e;
-    if (host_img_stride == h * host_pitch && host_pitch == dpitch) {
-      e = cudaMemcpyAsync(dev_buf, host_src + i0 * host_img_stride, (size_t)(m * dimg), cudaMemcpyHostToDevice, s);
-    } else {
-      e = cudaSuccess;
-      for (int64_t j = 0; j < m && e == cudaSuccess; ++j)
-        e = cudaMemcpy2DAsync(dev_buf + j * dimg, (size_t)dpitch, host_src + (i0 + j) * host_img_stride,
-                              (size_t)host_pitch, (size_t)w, (size_t)h, cudaMemcpyHostToDevice, s);
-    }
-    if (e != cudaSuccess) return cuda_fail(e);
+  auto stage = [&](uint8_t* dst, int64_t i0, int64_t m, cudaStream_t cs) -> cudaError_t {
+    if (host_img_stride == h * host_pitch && host_pitch == dpitch)
+      return cudaMemcpyAsync(dst, host_src + i0 * host_img_stride, (size_t)(m * dimg), cudaMemcpyHostToDevice, cs);
+    cudaError_t e = cudaSuccess;
+    for (int64_t j = 0; j < m && e == cudaSuccess; ++j)
+      e = cudaMemcpy2DAsync(dst + j * dimg, (size_t)dpitch, host_src + (i0 + j) * host_img_stride,
+                            (size_t)host_pitch, (size_t)w, (size_t)h, cudaMemcpyHostToDevice, cs);
+    return e;
+  };
+  auto compress_chunk = [&](const uint8_t* buf, int64_t i0, int64_t m) -> adct_status {
     for (int k = 0; k < n_r; ++k) {
-      st = adct_compress_psnr(dev_buf, m, h, w, dpitch, dimg, r_list[k], q, nullptr, ADCT_RECON_NONE, 0, 0,
-                              dev_sse + (int64_t)k * n + i0, stream);
-      if (st) return st;
+      adct_status st2 = adct_compress_psnr(buf, m, h, w, dpitch, dimg, r_list[k], q, nullptr, ADCT_RECON_NONE, 0,
+                                           0, dev_sse + (int64_t)k * n + i0, stream);
+      if (st2) return st2;
+    }
+    return ADCT_OK;
+  };
+  // Double-buffered pipeline: the host->device copy of chunk c+1 (own stream) overlaps the
+  // compress passes of chunk c (caller's stream).  Chunks of about n/8 images, two per buffer.
+  const int64_t half = cap / 2;
+  if (n >= 2 && half >= 1) {
+    const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(half, (n + 7) / 8));
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ready[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr}, start = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+      e = cudaEventCreateWithFlags(&ready[b], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+    // the staging buffer may still be read by work already queued on the caller's stream
+    if (e == cudaSuccess) e = cudaEventRecord(start, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, start, 0);
+    adct_status st2 = ADCT_OK;
+    int64_t c = 0;
+    for (int64_t i0 = 0; i0 < n && e == cudaSuccess && st2 == ADCT_OK; i0 += chunk, ++c) {
+      const int b = (int)(c & 1);
+      const int64_t m = std::min<int64_t>(chunk, n - i0);
+      uint8_t* buf = dev_buf + b * chunk * dimg;
+      if (c >= 2) e = cudaStreamWaitEvent(cs, freed[b], 0);  // chunk c-2's passes are done with buf
+      if (e == cudaSuccess) e = stage(buf, i0, m, cs);
+      if (e == cudaSuccess) e = cudaEventRecord(ready[b], cs);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ready[b], 0);
+      if (e == cudaSuccess) st2 = compress_chunk(buf, i0, m);
+      if (e == cudaSuccess && st2 == ADCT_OK) e = cudaEventRecord(freed[b], s);
+    }
+    // resources are released once their pending work completes (no host synchronisation)
+    for (int b = 0; b < 2; ++b) {
+      if (ready[b]) cudaEventDestroy(ready[b]);
+      if (freed[b]) cudaEventDestroy(freed[b]);
+    }
+    if (start) cudaEventDestroy(start);
+    if (cs) cudaStreamDestroy(cs);
+    if (e != cudaSuccess) return cuda_fail(e);
+    if (st2) return st2;
+  } else {
+    for (int64_t i0 = 0; i0 < n; i0 += cap) {
+      const int64_t m = std::min<int64_t>(cap, n - i0);
+      cudaError_t e = stage(dev_buf, i0, m, s);
+      if (e != cudaSuccess) return cuda_fail(e);
+      if ((st = compress_chunk(dev_buf, i0, m))) return st;
     }
   }
   // PSNR of every (r, image) into the second half of dev_sse, then one device->host copy

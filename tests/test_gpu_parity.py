@@ -309,16 +309,24 @@ def test_streams_and_determinism():
     assert np.allclose(c, host(a), rtol=1e-13)
 
 
-def test_end_to_end_host_entry_matches_device_path():
-    imgs = S.corpus_c2(6, 128, 128)
+@pytest.mark.parametrize("n,buf_imgs", [(6, 2), (6, 1), (17, 5), (17, 17), (1, 3)])
+def test_end_to_end_host_entry_matches_device_path(n, buf_imgs):
+    # buf_imgs >= 2: double-buffered copy/compute pipeline (chunks of ~n/8 images, two buffers);
+    # buf_imgs == 1 or n == 1: copy and passes alternate on the caller's stream
+    imgs = S.corpus_c2(n, 128, 128)
     rs = [1, 3, 6, 10, 15, 21, 28, 36]
     pinned = torch.from_numpy(imgs).pin_memory()
-    dev_buf = torch.empty((2 * 128 * 128,), dtype=torch.uint8, device="cuda")   # forces chunking
+    dev_buf = torch.empty((buf_imgs * 128 * 128,), dtype=torch.uint8, device="cuda")
     ps = A.compress_psnr_host(pinned, rs, dev_buf=dev_buf)
     torch.cuda.synchronize()
     for k, r in enumerate(rs):
-        want = O.psnr(O.compress_zonal_sse(imgs, r), 128 * 128)
-        assert np.all(np.abs(ps[k].numpy() - want) <= PSNR_TOL)
+        want_sse = O.compress_zonal_sse(imgs, r)
+        got = ps[k].numpy()
+        # a constant (lossless) image: exact zero on the GPU (+inf dB), float64 round-off (~1e-27,
+        # ~313 dB) in the oracle's literal matmuls -> compare the SSE there, PSNR elsewhere
+        lossless = want_sse <= 1e-9
+        assert np.all(np.isinf(got[lossless]))
+        assert np.all(np.abs(got[~lossless] - O.psnr(want_sse, 128 * 128)[~lossless]) <= PSNR_TOL)
 
 
 def test_launch_count_increments():
