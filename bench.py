@@ -72,6 +72,30 @@ def committed_traffic():
         return None
 
 
+def issue_roofline(tr, per_r_ms, tiles_per_launch, sm_mhz, dev):
+    """The compress pass is compute-bound: warp-instructions issued per second (the
+    committed ncu per-tile instruction count of each r's kernel x tiles / measured launch time)
+    against the issue peak of 1 warp-instruction per clock per SM sub-partition at the SM clock
+    sampled during the timed region.  The ALU and FMA pipes each retire 0.5 per clock."""
+    if not tr or not sm_mhz:
+        return None
+    import torch
+    per = {}
+    for name, v in tr.get("per_kernel", {}).items():
+        if "k_compress<" in name and "warp_instr_per_tile" in v:
+            per[int(name.split("k_compress<")[1].split(",")[0])] = v["warp_instr_per_tile"]
+    if not all(r in per for r in R_SET):
+        return None
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak = sms * 4 * sm_mhz * 1e6  # warp-instructions per second
+    ach = [per[r] * tiles_per_launch / (t * 1e-3) for r, t in zip(R_SET, per_r_ms)]
+    tot = sum(per[r] * tiles_per_launch for r in R_SET) / (sum(per_r_ms) * 1e-3)
+    return {"bound": "issue", "achieved": tot, "peak": peak, "unit": "warp-instr/s", "frac": tot / peak,
+            "per_r_frac": {str(r): a / peak for r, a in zip(R_SET, ach)},
+            "instr_source": "profiles/ncu_traffic.json warp_instr_per_tile (ncu --set full)",
+            "note": "compute roofline of the same kernel: 1 warp-instr/clk/SMSP at the sampled SM clock"}
+
+
 class ClockSampler:
     """Samples SM clock and throttle reasons with NVML during the timed region."""
 
@@ -257,6 +281,8 @@ def main():
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src, "kernel": "k_compress<r,ZONAL,NONE>",
                 "per_r_frac": {str(r): bytes_launch / (t * 1e-3) / 1e9 / peak for r, t in zip(R_SET, per_r)}}
+    clocks = clk.summary()
+    issue = issue_roofline(tr, per_r, n_loc * (H // 16) * (W // 256), clocks.get("sm_mhz"), dev)
 
     # ---- secondary (reported separately): Parseval sweep, one read for all 8 r
     energy = torch.empty((n_loc, 16), dtype=torch.int64, device=dev)
@@ -338,7 +364,7 @@ def main():
                            "parallelism": f"dp{world} (images sharded; one NCCL all-reduce of per-image SSE)",
                            "l2": "inputs 64 GiB >> 126 MB L2 (no flush needed)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clk.summary(), "fwd_only_c3": fwd_only, "parseval_sweep_f3": sweep,
+                "clocks": clocks, "issue_roofline": issue, "fwd_only_c3": fwd_only, "parseval_sweep_f3": sweep,
                 "mean_psnr_db": {str(r): float(np.mean(ps[k])) for k, r in enumerate(R_SET)}}
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -569,6 +569,26 @@ struct DiagParams {
   unsigned long long* energy;  // [n][16]
 };
 
+// weight groups of the anti-diagonals: position (k, l) -> index of W_kl among the distinct
+// weights of anti-diagonal k + l (in order of first appearance), and the weight of group g
+constexpr int diag_group_w(int s, int g) {
+  int ws[4] = {0, 0, 0, 0}, n = 0;
+  for (int k = 0; k < 8; ++k) {
+    const int l = s - k;
+    if (l < 0 || l > 7) continue;
+    const int W = wval(k, l);
+    bool seen = false;
+    for (int i = 0; i < n; ++i) seen = seen || ws[i] == W;
+    if (!seen) ws[n++] = W;
+  }
+  return g < n ? ws[g] : 0;
+}
+constexpr int diag_group(int k, int l) {
+  for (int g = 0; g < 4; ++g)
+    if (diag_group_w(k + l, g) == wval(k, l)) return g;
+  return -1;
+}
+
 template <int UNUSED = 0>
 __global__ void __launch_bounds__(WARPS * 32, 4)
     k_diag_energy(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ DiagParams p) {
@@ -601,13 +621,30 @@ __global__ void __launch_bounds__(WARPS * 32, 4)
     for (int i = 0; i < 8; ++i)
       pack_rows(lds64(tile + i * TILE_W + lane * 8), lds64(tile + (i + 8) * TILE_W + lane * 8), P[i]);
     uint32_t Y[8][8];
-    fwd2d<0x8000u, 64>(P, Y);  // lo lane biased by 2^15, hi lane exact
+    fwd2d<0u, 64>(P, Y);  // unbiased: lo lane = Y_A (two's complement), P - Y_A = Y_B * 2^16 exactly
+    // Per tile, exact u32 sums of Y^2 per (anti-diagonal s, weight W) group — 28 groups, at most 4
+    // positions x 2 blocks each, so a sum stays below 8 * 16320^2 < 2^32 — then one 64-bit
+    // multiply-add E_s += W * S per group.  Per coefficient pair: Y_A = sext16 (PRMT), Y_A^2 (IMAD),
+    // d = P - Y_A = Y_B 2^16 (IADD), Y_B^2 = hi(d * d) (IMAD.HI): 2 ALU + 2 FMA-pipe instructions.
+    uint32_t S[15][4];
+    static_for<15>([&](auto Sc) {
+      static_for<4>([&](auto Gc) { S[decltype(Sc)::value][decltype(Gc)::value] = 0u; });
+    });
     static_for<64>([&](auto KLc) {
       constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
-      constexpr int W = wval(k, l);
-      const int a = (int)(Y[k][l] & 0xFFFFu) - 32768;   // Y of block A
-      const int b = (int)Y[k][l] >> 16;                 // Y of block B
-      E[k + l] += (long long)a * (W * a) + (long long)b * (W * b);  // IMAD + IMAD.WIDE each, exact
+      constexpr int g = diag_group(k, l);
+      const uint32_t w = Y[k][l];
+      const int a = (int)(int16_t)(w & 0xFFFFu);      // sign-extended low lane: Y of block A
+      const int d = (int)(w - (uint32_t)a);           // Y of block B times 2^16
+      S[k + l][g] += (uint32_t)(a * a) + (uint32_t)__mulhi(d, d);
+    });
+    static_for<15>([&](auto Sc) {
+      constexpr int sd = decltype(Sc)::value;
+      static_for<4>([&](auto Gc) {
+        constexpr int g = decltype(Gc)::value;
+        if constexpr (diag_group_w(sd, g) > 0)
+          E[sd] += (long long)((unsigned long long)S[sd][g] * (unsigned)diag_group_w(sd, g));
+      });
     });
   });
   flush(cur);

@@ -45,7 +45,10 @@ if tj:
         scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         rd = float(d[hdr.index("dram__bytes_read.sum")]) * scale[raw[1][hdr.index("dram__bytes_read.sum")]]
         wr = float(d[hdr.index("dram__bytes_write.sum")]) * scale[raw[1][hdr.index("dram__bytes_write.sum")]]
-        per[name] = {"dram_bytes_per_px": (rd + wr) / px, "read_per_px": rd / px, "write_per_px": wr / px}
+        inst = float(d[hdr.index("smsp__inst_executed.sum")])
+        per[name] = {"dram_bytes_per_px": (rd + wr) / px, "read_per_px": rd / px, "write_per_px": wr / px,
+                     "warp_instr_per_tile": inst / tiles,
+                     "issue_active_pct": float(d[hdr.index("smsp__issue_active.avg.pct_of_peak_sustained_active")])}
     comp = [v["dram_bytes_per_px"] for k, v in per.items() if "k_compress" in k]
     with open(tj, "w") as f:
         json.dump({"source": f"ncu --set full, {int(tiles)} tiles of 4 KiB per launch "
