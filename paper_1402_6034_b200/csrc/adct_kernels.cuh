@@ -93,15 +93,16 @@ __device__ __forceinline__ void store_recon_row(uint8_t* base, int64_t pitch, in
       uint32_t u[8];
 #pragma unroll
       for (int n = 0; n < 8; ++n) {
-        // round_half_away(R / 576) then clamp: floor((R + 288.5) / 576) is exact for integer R
+        // round_half_away(R / 576) then clamp: floor((R + 288.5) / 576) is exact for integer R.
+        // floor of the clamped value through the 2^23 magic with a round-toward-zero add (FMA pipe):
+        // the low byte of the sum's bits is the integer part — no float->int conversion unit.
         const float xv = b ? x[n].y : x[n].x;
-        float t = S576 ? floorf((xv + 288.5f) * (1.0f / 576.0f)) : floorf(xv + 0.5f);
-        t = fminf(fmaxf(t, 0.f), 255.f);
-        u[n] = (uint32_t)t;
+        const float y = S576 ? (xv + 288.5f) * (1.0f / 576.0f) : xv + 0.5f;
+        u[n] = __float_as_uint(__fadd_rz(fminf(fmaxf(y, 0.f), 255.f), 8388608.0f));
       }
-      uint2 o;
-      o.x = u[0] | (u[1] << 8) | (u[2] << 16) | (u[3] << 24);
-      o.y = u[4] | (u[5] << 8) | (u[6] << 16) | (u[7] << 24);
+      uint2 o;  // pack the low bytes
+      o.x = __byte_perm(__byte_perm(u[0], u[1], 0x0040), __byte_perm(u[2], u[3], 0x0040), 0x5410);
+      o.y = __byte_perm(__byte_perm(u[4], u[5], 0x0040), __byte_perm(u[6], u[7], 0x0040), 0x5410);
       *reinterpret_cast<uint2*>(p + col) = o;
     }
   }
