@@ -141,6 +141,9 @@ void fill_quant_tables(Tables& t, int r, float q) {
       const float c = quant_recip(q, dval(k) * dval(l));
       t.w[k * 8 + l] = make_float2(qw, qw);
       t.c[k * 8 + l] = make_float2(c, c);
+      // per weight class (compile-time-r quantiser kernel): dequantiser weight and reciprocal
+      t.wc[wclass(k, l)] = (float)((double)q / sqrt(dd_host(k, l)));
+      t.cc[wclass(k, l)] = c;
     }
 }
 
@@ -323,6 +326,8 @@ adct_status adct_compress_psnr(const uint8_t* src, int64_t n, int64_t h, int64_t
   if (e != cudaSuccess) return cuda_fail(e);
   if (q > 0.f) {
     fill_quant_tables(p.tab, r, q);
+    if (recon_t == ADCT_RECON_NONE && r == 64)  // C4's case: compile-time mask, per-class constants
+      return launch_compress(k_compress<64, MODE_QUANT, REC_NONE>, 64, map, p, s);
     if (recon_t == ADCT_RECON_NONE) return launch_compress(k_compress<RT, MODE_QUANT, REC_NONE>, RT, map, p, s);
     if (recon_t == ADCT_RECON_F32) return launch_compress(k_compress<RT, MODE_QUANT, REC_F32>, RT, map, p, s);
     return launch_compress(k_compress<RT, MODE_QUANT, REC_U8>, RT, map, p, s);

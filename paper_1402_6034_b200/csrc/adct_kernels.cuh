@@ -117,7 +117,7 @@ __device__ __forceinline__ void store_recon_row(uint8_t* base, int64_t pitch, in
 // Forward half: packed SWAR coefficients Y (bias 0x80008000) of the two blocks of this lane.
 template <int R, int MODE>
 __device__ __forceinline__ void compress_fwd(const uint8_t* tile, int lane, uint32_t (&Y)[8][8]) {
-  constexpr int RF = (MODE == MODE_QUANT) ? RT : R;  // forward pruning level
+  constexpr int RF = R;  // forward pruning level (RT: runtime mask, all positions live)
   uint32_t P[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
@@ -146,7 +146,7 @@ __device__ __forceinline__ float2 err16(float2 F, FV<true> r) { return f2fma(F, 
 template <int R, int MODE, int RECON, int F16 = 0, bool GROUPED = false>
 __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const uint8_t* tile, int lane,
                                                const CompressParams& p, int img, int ty, int tx) {
-  constexpr int RF = (MODE == MODE_QUANT) ? RT : R;
+  constexpr int RF = R;
   static_assert(F16 == 0 || (MODE == MODE_ZONAL && RECON == REC_NONE && RF < RT), "f16 error route: zonal SSE only");
   float2 V[64];
   static_for<64>([&](auto KLc) {
@@ -164,8 +164,14 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
         const float2 y = f2add(biased_pair(Y[k][l]), f2(-KF));          // Y, exact
         // 1.5*2^23 + RN(Y c'): c' lies strictly above 1/(q sqrt dd), so exact ties of Z/q round
         // away from zero and no product Y c' is itself a tie (reading R10)
-        const float2 t = f2fma(y, p.tab.c[kl], f2(12582912.0f));
-        V[kl] = __fmul2_rn(f2add(t, f2(-12582912.0f)), p.tab.w[kl]);     // q k / sqrt(dd) (M folded)
+        if constexpr (RF < RT) {  // compile-time mask: per-class scalars (q / sqrt dd, c')
+          constexpr int c = wclass(k, l);
+          const float2 t = f2fma(y, f2(p.tab.cc[c]), f2(12582912.0f));
+          V[kl] = __fmul2_rn(f2add(t, f2(-12582912.0f)), f2(p.tab.wc[c]));
+        } else {
+          const float2 t = f2fma(y, p.tab.c[kl], f2(12582912.0f));
+          V[kl] = __fmul2_rn(f2add(t, f2(-12582912.0f)), p.tab.w[kl]);   // q k / sqrt(dd) (M folded)
+        }
       }
     }
   });
@@ -264,13 +270,17 @@ constexpr int compress_f16_rows(int R) { return R <= 3 ? 8 : 0; }
 #define ADCT_GROUPED 0
 #endif
 constexpr bool compress_grouped(int R) { return ADCT_GROUPED || (R >= 15 && R < ADCT_RESID_FROM); }
+// runtime-mask / quantiser / reconstruction kernels (all 64 coefficients live)
+#ifndef ADCT_MINB_RT
+#define ADCT_MINB_RT 2  // measured: 5-17 % faster than 3 (no spills), profiles/r01_variants_session3.txt
+#endif
 // measured on B200 (profiles/r01_tune_minb.txt): small r wants occupancy, mid r registers
 constexpr int compress_minb(int R) {
   return compress_resid_r(R) ? 4 : (R == 1 ? 6 : (R <= 3 ? 5 : (R <= 6 ? 4 : 3)));
 }
 
-template <int R, int MODE, int RECON, int ST = compress_stages((MODE == MODE_QUANT) ? RT : R),
-          int MINB = (MODE == MODE_ZONAL && RECON == REC_NONE) ? compress_minb(R) : 3,
+template <int R, int MODE, int RECON, int ST = compress_stages(R),
+          int MINB = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_minb(R) : ADCT_MINB_RT,
           bool RES = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT && compress_resid_r(R)),
           int F16 = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_f16_rows(R) : 0,
           bool GRP = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_grouped(R) : false>
