@@ -464,3 +464,54 @@ def test_uqi_ape_proposed_vs_dct_end_to_end():
         om_p = O.compress_zonal_sse(imgs, r).mean() / 128 ** 2
         om_d = O.compress_zonal_sse(imgs, r, O.dct_matrix()).mean() / 128 ** 2
         assert abs(O.ape(mse_p, mse_d) - O.ape(om_p, om_d)) <= 1e-2
+
+
+# ---- out-of-bounds write guards (compute-sanitizer is not available on this GPU pool; every
+# output buffer is a window of a larger canary-filled buffer, and nothing outside may change)
+def _window(n, h, w, dtype, fill, pad_rows=8, pad_cols=32):
+    """[n, h, w] view with 16-byte pitch into a canary buffer of (n + 1) x (h + pad) x (w + pad)."""
+    es = torch.empty((), dtype=dtype).element_size()
+    wp = -(-(w + pad_cols) * es // 16) * 16 // es
+    big = torch.full((n + 1, h + pad_rows, wp), fill, dtype=dtype, device="cuda")
+    return big, big[:n, :h, :w]
+
+
+def _outside(big, n, h, w):
+    m = torch.ones_like(big, dtype=torch.bool)
+    m[:n, :h, :w] = False
+    return big[m]
+
+
+@pytest.mark.parametrize("n,h,w", [(3, 40, 264), (1, 8, 8), (2, 24, 520), (2, 16, 256)])
+def test_no_writes_outside_outputs(n, h, w):
+    x = dev(rng.integers(0, 256, (n, h, w), dtype=np.uint8))
+    canary_f, canary_u, canary_i = -12345.5, 77, -4321
+    # per-image arrays: a canary tail after the n entries
+    sse_big = torch.full((n + 8,), canary_f, dtype=torch.float64, device="cuda")
+    for r, q in [(1, 0.0), (10, 0.0), (21, 0.0), (36, 0.0), (64, 16.0), (20, 5.0)]:
+        A.compress_psnr(x, r, q=q, sse=sse_big[:n])
+        assert torch.all(sse_big[n:] == canary_f)
+    for kind, dt, fill in [("f32", torch.float32, canary_f), ("u8", torch.uint8, canary_u)]:
+        for r, q in [(10, 0.0), (36, 0.0), (64, 16.0)]:
+            big, win = _window(n, h, w, dt, fill)
+            A.compress_psnr(x, r, q=q, recon=kind, recon_out=win)
+            assert torch.all(_outside(big, n, h, w) == fill), (kind, r, q)
+    for coef, dt, fill in [("i16", torch.int16, canary_i), ("i32", torch.int32, canary_i), ("f32", torch.float32, canary_f)]:
+        big, win = _window(n, h, w, dt, fill)
+        A.forward(x, r=15, coef=coef, out=win)
+        assert torch.all(_outside(big, n, h, w) == fill), coef
+    y = A.forward(x)
+    for out, dt, fill in [("f32", torch.float32, canary_f), ("u8", torch.uint8, canary_u)]:
+        big, win = _window(n, h, w, dt, fill)
+        A.inverse(y, r=28, out=out, dst=win)
+        assert torch.all(_outside(big, n, h, w) == fill), out
+    big, win = _window(n, h, w, torch.float32, canary_f)
+    A.compress_psnr_dense(x, 10, "dct", recon=True, recon_out=win)
+    assert torch.all(_outside(big, n, h, w) == canary_f)
+    e_big = torch.full((n + 2, 16), canary_i, dtype=torch.int64, device="cuda")
+    A.diag_energy(x, energy=e_big[:n])
+    assert torch.all(e_big[n:] == canary_i)
+    u_big = torch.full((n + 4,), canary_f, dtype=torch.float64, device="cuda")
+    A.uqi(x, A.compress_psnr(x, 10, recon="f32")[1], out=u_big[:n])
+    assert torch.all(u_big[n:] == canary_f)
+    torch.cuda.synchronize()
