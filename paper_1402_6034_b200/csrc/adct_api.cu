@@ -65,6 +65,23 @@ adct_status make_u8_map(CUtensorMap* map, const uint8_t* src, int64_t n, int64_t
   return ADCT_OK;
 }
 
+// int16 coefficient plane (adct_inverse's TMA path): same box, 2-byte elements (copied as UINT16 —
+// TMA moves bytes; the kernel reinterprets them)
+adct_status make_i16_map(CUtensorMap* map, const void* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                         int64_t img_stride) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) return cuda_fail(cudaErrorNotSupported);
+  cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
+  cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)img_stride};
+  cuuint32_t box[3] = {TILE_W, TILE_H, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(src), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cuda_fail(cudaErrorInvalidValue);
+  return ADCT_OK;
+}
+
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 adct_status check_geom(int64_t n, int64_t h, int64_t w) {
@@ -150,9 +167,9 @@ void fill_quant_tables(Tables& t, int r, float q) {
 
 template <class K, class P>
 adct_status launch_tma_kernel(K kern, const CUtensorMap& map, const P& params_in, int64_t tiles,
-                              cudaStream_t stream, int stages = STAGES) {
+                              cudaStream_t stream, int stages = STAGES, int tile_bytes = TILE_BYTES) {
   P params = params_in;
-  const int smem = WARPS * stages * TILE_BYTES + WARPS * stages * 8;
+  const int smem = WARPS * stages * tile_bytes + WARPS * stages * 8;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return cuda_fail(e);
   int dev = 0, sms = 0, occ = 0;
@@ -274,7 +291,16 @@ adct_status adct_inverse(const void* coef, adct_coef_t coef_t, int64_t n, int64_
       if (zz_host(k, l) < r)
         m = (coef_t == ADCT_COEF_F32) ? (float)(576.0 / sqrt(dd_host(k, l))) : (float)wval(k, l);
       p.tab.w[k * 8 + l] = make_float2(m, m);
+      p.tab.c[k * 8 + l] = make_float2(-KF * m, -KF * m);  // TMA int16 path: debias of the magic pair
     }
+  cudaStream_t s0 = (cudaStream_t)stream;
+  if (coef_t == ADCT_COEF_I16) {  // staged by TMA through the warp rings (HBM-bound path)
+    CUtensorMap map;
+    if ((st = make_i16_map(&map, coef, n, h, w, coef_pitch, coef_img_stride))) return st;
+    return dst_t == ADCT_RECON_F32
+               ? launch_tma_kernel(k_inverse_i16<REC_F32>, map, p, p.tiles, s0, 2, 2 * TILE_BYTES)
+               : launch_tma_kernel(k_inverse_i16<REC_U8>, map, p, p.tiles, s0, 2, 2 * TILE_BYTES);
+  }
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -61,6 +61,7 @@ struct ForwardParams {
 struct InverseParams {
   TileGeo geo;
   int64_t tiles;
+  int cshift;  // TMA (int16) path: log2 tiles per scheduling chunk
   int h, w;
   const uint8_t* coef;
   int64_t coef_pitch, coef_img_stride;
@@ -449,6 +450,52 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_inverse(const __grid_constant
       store_recon_row<RECON, true>(dbase, p.dst_pitch, p.h, p.w, ty * TILE_H + I, col, xr);
     });
   }
+}
+
+// Inverse from an int16 coefficient plane staged by TMA (16 x 256 coefficients = 8 KiB per warp
+// tile, the same ring as the compress kernels): a lane's two blocks are rows 0-7 / 8-15 of its
+// 8-column slice.  Coefficients become biased float pairs (xor 0x80008000, PRMT pairing A/B, the
+// 2^23 magic) weighted by the runtime mask table, then the f32x2 inverse and the store.
+template <int RECON>
+__global__ void __launch_bounds__(WARPS * 32, 3)
+    k_inverse_i16(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ InverseParams p) {
+  constexpr int TB = 2 * TILE_BYTES;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  uint8_t* ring = smem + warp * (2 * TB);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * 2 * TB) + warp * 2;
+  const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
+  tma_ring_loop_u<2, TB>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
+                     [&](const uint8_t* tile, int img, int ty, int tx) {
+    float2 V[64];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint4 a = *reinterpret_cast<const uint4*>(tile + (k * TILE_W + lane * 8) * 2);
+      const uint4 b = *reinterpret_cast<const uint4*>(tile + ((k + 8) * TILE_W + lane * 8) * 2);
+      const uint32_t wa[4] = {a.x ^ 0x80008000u, a.y ^ 0x80008000u, a.z ^ 0x80008000u, a.w ^ 0x80008000u};
+      const uint32_t wb[4] = {b.x ^ 0x80008000u, b.y ^ 0x80008000u, b.z ^ 0x80008000u, b.w ^ 0x80008000u};
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int kl = k * 8 + 2 * m + h;
+          const uint32_t P = __byte_perm(wa[m], wb[m], h ? 0x7632 : 0x5410);  // (A + 2^15) | (B + 2^15) << 16
+          V[kl] = f2fma(biased_pair(P), f2(p.tab.w[kl].x), f2(p.tab.c[kl].x));  // w Y (0 if masked)
+        }
+      }
+    }
+    const int col = tx * TILE_W + lane * 8;
+    uint8_t* dbase = p.dst + (int64_t)img * p.dst_img_stride;
+    inverse2d<RT>(V, [&](auto Ic, auto row) {
+      constexpr int I = decltype(Ic)::value;
+      float2 xr[8];
+      static_for<8>([&](auto Nc) {
+        constexpr int N = decltype(Nc)::value;
+        xr[N] = val(cuda::std::get<N>(row));
+      });
+      store_recon_row<RECON, true>(dbase, p.dst_pitch, p.h, p.w, ty * TILE_H + I, col, xr);
+    });
+  });
 }
 
 // ------------------------------------------------------------------------------------------
