@@ -462,7 +462,7 @@ adct_status adct_diag_energy(const uint8_t* src, int64_t n, int64_t h, int64_t w
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(energy, 0, sizeof(uint64_t) * 16 * (size_t)n, s);
   if (e != cudaSuccess) return cuda_fail(e);
-  return launch_tma_kernel(k_diag_energy<0>, map, p, p.tiles, s);
+  return launch_tma_kernel(k_diag_energy<0>, map, p, p.tiles, s, DIAG_ST);
 }
 
 adct_status adct_sweep_psnr(const uint64_t* energy, int64_t n, int64_t pixels, const int* r_list, int n_r, double* sse,

@@ -647,13 +647,20 @@ constexpr int diag_group(int k, int l) {
   return -1;
 }
 
+#ifndef ADCT_DIAG_ST
+#define ADCT_DIAG_ST 2
+#endif
+#ifndef ADCT_DIAG_MINB
+#define ADCT_DIAG_MINB 3
+#endif
+constexpr int DIAG_ST = ADCT_DIAG_ST, DIAG_MINB = ADCT_DIAG_MINB;  // ring depth, CTAs per SM (measured: 2/3 best, 0.53 vs 0.46 of HBM for 3/4)
 template <int UNUSED = 0>
-__global__ void __launch_bounds__(WARPS * 32, 4)
+__global__ void __launch_bounds__(WARPS * 32, DIAG_MINB)
     k_diag_energy(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ DiagParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  uint8_t* ring = smem + warp * (STAGES * TILE_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * STAGES * TILE_BYTES) + warp * STAGES;
+  uint8_t* ring = smem + warp * (DIAG_ST * TILE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * DIAG_ST * TILE_BYTES) + warp * DIAG_ST;
   const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
   int cur = -1;
   long long E[15];
@@ -669,7 +676,7 @@ __global__ void __launch_bounds__(WARPS * 32, 4)
       E[s] = 0;
     }
   };
-  tma_ring_loop_u<STAGES>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
+  tma_ring_loop_u<DIAG_ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {
       flush(cur);
       cur = img;
