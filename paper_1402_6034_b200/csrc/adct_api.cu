@@ -256,9 +256,9 @@ adct_status adct_forward(const uint8_t* src, int64_t n, int64_t h, int64_t w, in
       p.sc[k * 8 + l] = (zz_host(k, l) < r) ? (float)(1.0 / sqrt(dd_host(k, l))) : 0.f;
   cudaStream_t s = (cudaStream_t)stream;
   switch (coef_t) {
-    case ADCT_COEF_I16: return launch_tma_kernel(k_forward<OUT_I16>, map, p, p.tiles, s);
-    case ADCT_COEF_I32: return launch_tma_kernel(k_forward<OUT_I32>, map, p, p.tiles, s);
-    default: return launch_tma_kernel(k_forward<OUT_F32>, map, p, p.tiles, s);
+    case ADCT_COEF_I16: return launch_tma_kernel(k_forward<OUT_I16>, map, p, p.tiles, s, FWD_ST);
+    case ADCT_COEF_I32: return launch_tma_kernel(k_forward<OUT_I32>, map, p, p.tiles, s, FWD_ST);
+    default: return launch_tma_kernel(k_forward<OUT_F32>, map, p, p.tiles, s, FWD_ST);
   }
 }
 

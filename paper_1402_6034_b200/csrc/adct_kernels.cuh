@@ -377,15 +377,22 @@ __device__ __forceinline__ void tile_forward(const uint8_t* tile, int lane, cons
   }
 }
 
+#ifndef ADCT_FWD_ST
+#define ADCT_FWD_ST 3
+#endif
+#ifndef ADCT_FWD_MINB
+#define ADCT_FWD_MINB 3
+#endif
+constexpr int FWD_ST = ADCT_FWD_ST, FWD_MINB = ADCT_FWD_MINB;  // ring depth, CTAs per SM
 template <int OUT>
-__global__ void __launch_bounds__(WARPS * 32, 3)
+__global__ void __launch_bounds__(WARPS * 32, FWD_MINB)
     k_forward(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ ForwardParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  uint8_t* ring = smem + warp * (STAGES * TILE_BYTES);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * STAGES * TILE_BYTES) + warp * STAGES;
+  uint8_t* ring = smem + warp * (FWD_ST * TILE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * FWD_ST * TILE_BYTES) + warp * FWD_ST;
   const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
-  tma_ring_loop_u<STAGES>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
+  tma_ring_loop_u<FWD_ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
     tile_forward<OUT>(tile, lane, p, img, ty, tx);
   });
 }
