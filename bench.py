@@ -284,6 +284,28 @@ def main():
     clocks = clk.summary()
     issue = issue_roofline(tr, per_r, n_loc * (H // 16) * (W // 256), clocks.get("sm_mhz"), dev)
 
+    # ---- secondary (SURVEY F3 with the inverse, reported separately): fused multi-r kernel —
+    # one read and one forward per tile, then every r's zonal step, inverse and per-pixel error
+    multi_sse = torch.empty((len(R_SET), n_loc), dtype=torch.float64, device=dev)
+    for _ in range(2):
+        A.compress_psnr_multi(x, R_SET, sse=multi_sse)
+    torch.cuda.synchronize()
+    m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    m0.record(stream)
+    for _ in range(a.steps):
+        A.compress_psnr_multi(x, R_SET, sse=multi_sse)
+    m1.record(stream)
+    torch.cuda.synchronize()
+    mms = max_over_ranks(m0.elapsed_time(m1) / a.steps, dev)
+    fused = {"what": "adct_compress_psnr_multi: one read + one forward per tile, then for every r the zonal "
+                     "step, inverse and per-pixel error (each r's own arithmetic); NOT the headline, which runs "
+                     "the 8 r-passes independently",
+             "gpix_passes_s": world * n_loc * H * W * len(R_SET) / (mms * 1e-3) / 1e9, "ms": mms,
+             "speedup_vs_independent_passes": (ms_step / mms),
+             "max_rel_diff_vs_independent_sse": float(((multi_sse - sse[:, lo:hi]).abs() /
+                                                       sse[:, lo:hi].clamp_min(1e-30)).max().item())}
+    del multi_sse
+
     # ---- secondary (reported separately): Parseval sweep, one read for all 8 r
     energy = torch.empty((n_loc, 16), dtype=torch.int64, device=dev)
     for _ in range(2):
@@ -365,6 +387,7 @@ def main():
                            "l2": "inputs 64 GiB >> 126 MB L2 (no flush needed)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clocks, "issue_roofline": issue, "fwd_only_c3": fwd_only, "parseval_sweep_f3": sweep,
+                "fused_multi_r_c5": fused,
                 "mean_psnr_db": {str(r): float(np.mean(ps[k])) for k, r in enumerate(R_SET)}}
         print(json.dumps(line), flush=True)
     if world > 1:

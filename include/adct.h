@@ -120,6 +120,18 @@ adct_status adct_psnr(const double* sse, int64_t count, int64_t pixels, double* 
                       adct_stream_t stream);
 
 /*
+ * adct_compress_psnr_multi — several zonal r over the same images (q = 0, SSE only):
+ * sse[k * n + i] = adct_compress_psnr's SSE of image i at r = r_list[k] (OVERWRITTEN).
+ * For BASELINE C5's set {1, 3, 6, 10, 15, 21, 28, 36} (any order) one fused kernel reads each tile
+ * once, runs the forward once and, for every r, the zonal step, inverse and per-pixel error with
+ * that r's own arithmetic (results identical to the single-r calls up to fp64 summation order);
+ * any other set runs independent passes.  n_r in [1, 64]; sse device double[n_r * n].
+ */
+adct_status adct_compress_psnr_multi(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                                     int64_t img_stride, const int* r_list, int n_r, double* sse,
+                                     adct_stream_t stream);
+
+/*
  * adct_compress_psnr_host — end-to-end entry with HOST buffers: copies the images from host
  * memory (pinned recommended; host_src with host_pitch / host_img_stride in bytes) through the
  * caller's device staging buffer `dev_buf` (dev_buf_bytes >= one image of h * w bytes; images are

@@ -3,11 +3,12 @@
 Python surface = the C ABI in include/adct.h (same names, argument marshalling only):
 forward, inverse, compress_psnr, psnr, compress_psnr_host.  See DESIGN.md.
 """
-from ._lib import (AdctError, compress_psnr, compress_psnr_dense, compress_psnr_host, diag_energy,  # noqa: F401
+from ._lib import (AdctError, compress_psnr, compress_psnr_dense, compress_psnr_host, compress_psnr_multi,  # noqa: F401
+                   diag_energy,
                    empty_plane, sweep_psnr,
                    forward, inverse, launch_count, load, psnr, quant_reciprocals, to_device,
                    transform_matrix, uqi, version)
 
 __all__ = ["forward", "inverse", "compress_psnr", "psnr", "compress_psnr_host", "load", "launch_count",
            "version", "AdctError", "empty_plane", "to_device", "quant_reciprocals",
-           "compress_psnr_dense", "transform_matrix", "diag_energy", "sweep_psnr", "uqi"]
+           "compress_psnr_dense", "transform_matrix", "diag_energy", "sweep_psnr", "uqi", "compress_psnr_multi"]

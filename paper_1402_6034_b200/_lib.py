@@ -28,6 +28,7 @@ SIGNATURES = {
     "adct_psnr": (_i32, [_vp, _i64, _i64, _vp, _vp]),
     "adct_compress_psnr_host": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _i32, _f32, _vp, _i64,
                                        _vp, _vp, _vp]),
+    "adct_compress_psnr_multi": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _i32, _vp, _vp]),
     "adct_quant_reciprocals": (_i32, [_f32, _vp]),
     "adct_compress_psnr_dense": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _vp, _i64, _i64,
                                         _vp, _vp]),
@@ -252,6 +253,24 @@ def compress_psnr(x, r: int, q: float = 0.0, recon: str | None = None, sse=None,
     _check(load().adct_compress_psnr(p, n, h, w, pitch, istr, r, float(q), rp, RECON[recon], rpitch, ristr,
                                      sse.data_ptr(), _stream(stream)), "adct_compress_psnr")
     return (sse, recon_out) if recon not in (None, "none") else sse
+
+
+def compress_psnr_multi(x, r_list, sse=None, stream=None):
+    """adct_compress_psnr_multi: SSE [len(r_list), n] of the zonal pass for every r (q = 0).
+
+    BASELINE C5's r set runs as one fused kernel (one read, one forward, every r's inverse and
+    per-pixel error); other sets run independent passes."""
+    torch = _torch()
+    p, n, h, w, pitch, istr = _plane(x, 1)
+    nr = len(r_list)
+    if sse is None:
+        sse = torch.empty((nr, n), dtype=torch.float64, device=x.device)
+    if not sse.is_contiguous() or tuple(sse.shape) != (nr, n):
+        raise ValueError("sse must be a contiguous [len(r_list), n] float64 tensor")
+    rl = (ctypes.c_int * nr)(*[int(v) for v in r_list])
+    _check(load().adct_compress_psnr_multi(p, n, h, w, pitch, istr, rl, nr, sse.data_ptr(), _stream(stream)),
+           "adct_compress_psnr_multi")
+    return sse
 
 
 def psnr(sse, pixels: int, out=None, stream=None):

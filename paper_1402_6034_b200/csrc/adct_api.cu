@@ -537,6 +537,51 @@ adct_status adct_psnr(const double* sse, int64_t count, int64_t pixels, double* 
   return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
 }
 
+adct_status adct_compress_psnr_multi(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                                     int64_t img_stride, const int* r_list, int n_r, double* sse,
+                                     adct_stream_t stream) {
+  adct_status st = check_geom(n, h, w);
+  if (st) return st;
+  if (!r_list || n_r < 1 || n_r > 64 || !sse) return ADCT_EINVAL;
+  for (int k = 0; k < n_r; ++k)
+    if (r_list[k] < 1 || r_list[k] > 64) return ADCT_EINVAL;
+  if ((st = check_plane(src, h, w, pitch, img_stride))) return st;
+  if ((uintptr_t)sse & 7u) return ADCT_EALIGN;
+  // the compiled set (BASELINE C5's r, any order, each once) -> one fused kernel
+  int rowmap[8];
+  bool fused = (n_r == RSetC5::n);
+  for (int k = 0; fused && k < RSetC5::n; ++k) {
+    int hit = -1;
+    for (int i = 0; i < n_r; ++i)
+      if (r_list[i] == RSetC5::r[k]) hit = (hit < 0) ? i : -2;
+    fused = hit >= 0;
+    rowmap[k] = hit;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!fused) {  // any other set: independent passes
+    for (int k = 0; k < n_r; ++k)
+      if ((st = adct_compress_psnr(src, n, h, w, pitch, img_stride, r_list[k], 0.f, nullptr, ADCT_RECON_NONE, 0, 0,
+                                   sse + (int64_t)k * n, stream)))
+        return st;
+    return ADCT_OK;
+  }
+  CUtensorMap map;
+  if ((st = make_u8_map(&map, src, n, h, w, pitch, img_stride))) return st;
+  CompressParams p;
+  memset(&p, 0, sizeof(p));
+  p.geo = make_geo(h, w);
+  p.tiles = p.geo.per_img * n;
+  p.h = (int)h;
+  p.w = (int)w;
+  p.sse = sse;
+  p.sse_stride = n;
+  for (int k = 0; k < 8; ++k) p.rowmap[k] = rowmap[k];
+  fill_zonal_tables(p.tab, 64);  // per-class weights (the compile-time masks need nothing else)
+  cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(double) * (size_t)(n * n_r), s);
+  if (e != cudaSuccess) return cuda_fail(e);
+  return launch_compress(multi_kernel_c5(), 1, map, p, s);
+}
+
 adct_status adct_compress_psnr_host(const uint8_t* host_src, int64_t n, int64_t h, int64_t w,
                                     int64_t host_pitch, int64_t host_img_stride, const int* r_list, int n_r,
                                     float q, uint8_t* dev_buf, int64_t dev_buf_bytes, double* dev_sse,

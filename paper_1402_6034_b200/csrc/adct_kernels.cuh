@@ -42,6 +42,8 @@ struct CompressParams {
   double* sse;
   uint8_t* recon;
   int64_t recon_pitch, recon_img_stride;
+  int64_t sse_stride;  // multi-r kernel: distance between the per-r SSE rows (doubles)
+  int rowmap[8];       // multi-r kernel: output row of the k-th r of the compiled set
   Tables tab;
 };
 
@@ -835,7 +837,69 @@ __global__ void __launch_bounds__(256) k_uqi(const __grid_constant__ UqiParams p
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// Fused multi-r sweep (with the inverse): one read and ONE forward per tile, then
+// for every r of the set the full zonal step, inverse and per-pixel error (each r exactly the
+// arithmetic of its own k_compress<r> instantiation: direct / grouped / residual form, f16 route).
+// The forward is identical for every r, so computing it once is not work skipped; every r's
+// reconstruction error is still computed pixel by pixel.  Reported separately from the headline
+// (which runs the r-passes independently).  r are processed in descending order so the packed
+// coefficients of the high anti-diagonals die early (register pressure).
+// ------------------------------------------------------------------------------------------
+struct RSetC5 {
+  static constexpr int n = 8;
+  static constexpr int r[8] = {36, 28, 21, 15, 10, 6, 3, 1};
+};
+
+#ifndef ADCT_MULTI_MINB
+#define ADCT_MULTI_MINB 2
+#endif
+template <class RS>
+__global__ void __launch_bounds__(WARPS * 32, ADCT_MULTI_MINB)
+    k_compress_multi(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CompressParams p) {
+  constexpr int ST = 2;
+  constexpr double kSseScale = 1.0 / 331776.0;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  uint8_t* ring = smem + warp * (ST * TILE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * ST * TILE_BYTES) + warp * ST;
+  const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
+  int cur = -1;
+  double acc[RS::n];
+#pragma unroll
+  for (int k = 0; k < RS::n; ++k) acc[k] = 0.0;
+  auto flush = [&]() {
+#pragma unroll
+    for (int k = 0; k < RS::n; ++k) {
+      const double v = warp_sum(acc[k]);
+      if (lane == 0 && cur >= 0) atomicAdd(p.sse + (int64_t)p.rowmap[k] * p.sse_stride + cur, v * kSseScale);
+      acc[k] = 0.0;
+    }
+  };
+  tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
+                      [&](const uint8_t* tile, int img, int ty, int tx) {
+    if (img != cur) {  // warp-uniform
+      flush();
+      cur = img;
+    }
+    uint32_t Y[8][8];
+    compress_fwd<64, MODE_ZONAL>(tile, lane, Y);  // all positions; outputs no r uses are dead code
+    static_for<RS::n>([&](auto Kc) {
+      constexpr int k = decltype(Kc)::value, R = RS::r[k];
+      float2 e2;
+      if constexpr (compress_resid_r(R))
+        e2 = compress_resid<R, compress_grouped(R)>(Y, p);
+      else
+        e2 = compress_inv<R, MODE_ZONAL, REC_NONE, compress_f16_rows(R), compress_grouped(R)>(Y, tile, lane, p,
+                                                                                              img, ty, tx);
+      acc[k] += (double)e2.x + (double)e2.y;
+    });
+  });
+  flush();
+}
+
 typedef void (*CompressKernel)(CUtensorMap, CompressParams);
+CompressKernel multi_kernel_c5();  // k_compress_multi<RSetC5>, instantiated in multi_r.cu
 // zonal kernels k_compress<r, ZONAL, RECON_NONE>, instantiated in zonal_part*.cu (4 TUs)
 CompressKernel zonal_kernel(int r);
 

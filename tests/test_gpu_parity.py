@@ -515,3 +515,24 @@ def test_no_writes_outside_outputs(n, h, w):
     A.uqi(x, A.compress_psnr(x, 10, recon="f32")[1], out=u_big[:n])
     assert torch.all(u_big[n:] == canary_f)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("order", [(1, 3, 6, 10, 15, 21, 28, 36), (36, 1, 21, 3, 28, 6, 15, 10), (1, 2, 64)])
+def test_compress_multi_matches_single_passes(order):
+    # C5's set in any order runs the fused kernel (one forward, every r's inverse and error);
+    # other sets fall back to single passes.  Both must equal the single-r calls / the oracle.
+    imgs = S.corpus_c2(7, 48, 520)
+    x = dev(imgs)
+    got = host(A.compress_psnr_multi(x, order))
+    for k, r in enumerate(order):
+        single = host(A.compress_psnr(x, r))
+        assert np.allclose(got[k], single, rtol=1e-12, atol=1e-12), r
+        check_sse(got[k], O.compress_zonal_sse(imgs, r), 48 * 520)
+
+
+def test_compress_multi_c5_full_size_sampled():
+    x = S.device_mixed(6, 4096, 4096, seed=3)
+    rs = (1, 3, 6, 10, 15, 21, 28, 36)
+    got = host(A.compress_psnr_multi(x, rs))
+    for k, r in enumerate(rs):
+        assert np.allclose(got[k], host(A.compress_psnr(x, r)), rtol=1e-12), r
