@@ -272,14 +272,14 @@ constexpr int compress_f16_rows(int R) { return R <= 3 ? 8 : 0; }
 #ifndef ADCT_GROUPED
 #define ADCT_GROUPED 0
 #endif
-constexpr bool compress_grouped(int R) { return ADCT_GROUPED || (R >= 15 && R < ADCT_RESID_FROM); }
+constexpr bool compress_grouped(int R) { return ADCT_GROUPED || (R >= 6 && R < ADCT_RESID_FROM); }
 // runtime-mask / quantiser / reconstruction kernels (all 64 coefficients live)
 #ifndef ADCT_MINB_RT
 #define ADCT_MINB_RT 2  // measured: 5-17 % faster than 3 (no spills), profiles/r01_variants_session3.txt
 #endif
 // measured on B200 (profiles/r01_tune_minb.txt): small r wants occupancy, mid r registers
 constexpr int compress_minb(int R) {
-  return compress_resid_r(R) ? 4 : (R == 1 ? 6 : (R <= 3 ? 5 : (R <= 6 ? 4 : 3)));
+  return compress_resid_r(R) ? 4 : (R == 1 ? 6 : (R <= 3 ? 5 : (R <= 15 ? 4 : 3)));
 }
 
 template <int R, int MODE, int RECON, int ST = compress_stages(R),
