@@ -143,3 +143,18 @@ def test_sweep_validation():
     rl = (ctypes.c_int * 1)(10)
     assert lib.adct_sweep_psnr(16, 0, 64, rl, 1, 32, 48, None) == E
     assert lib.adct_diag_energy(16, 1, 8, 16, 16, 128, 0, None) == E
+
+
+def test_multi_and_geometry_limits_validation():
+    lib = A.load()
+    E, AL = _lib.ADCT_EINVAL, _lib.ADCT_EALIGN
+    rl = (ctypes.c_int * 3)(1, 10, 36)
+    bad = (ctypes.c_int * 2)(0, 10)
+    assert lib.adct_compress_psnr_multi(16, 1, 8, 16, 16, 128, rl, 0, 64, None) == E     # n_r = 0
+    assert lib.adct_compress_psnr_multi(16, 1, 8, 16, 16, 128, bad, 2, 64, None) == E    # r = 0
+    assert lib.adct_compress_psnr_multi(16, 1, 8, 16, 16, 128, None, 3, 64, None) == E   # no list
+    assert lib.adct_compress_psnr_multi(16, 1, 8, 16, 16, 128, rl, 3, 0, None) == E      # no sse
+    assert lib.adct_compress_psnr_multi(16, 1, 8, 16, 16, 128, rl, 3, 68, None) == AL    # misaligned sse
+    # the device tile cursors are 32-bit: more than 2^30 tiles of 16 x 256 px in one call is rejected
+    n_big = (1 << 30) // (2 * 16) + 1                                                     # 512 x 4096 images
+    assert lib.adct_compress_psnr(16, n_big, 512, 4096, 4096, 512 * 4096, 10, 0.0, 0, 0, 0, 0, 64, None) == E
