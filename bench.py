@@ -280,6 +280,7 @@ def main():
         traffic = tr["dram_bytes_per_px"] * bytes_launch
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src, "kernel": "k_compress<r,ZONAL,NONE>",
+                "frac_vs_spec_8000": achieved / 8000.0,
                 "per_r_frac": {str(r): bytes_launch / (t * 1e-3) / 1e9 / peak for r, t in zip(R_SET, per_r)}}
     clocks = clk.summary()
     issue = issue_roofline(tr, per_r, n_loc * (H // 16) * (W // 256), clocks.get("sm_mhz"), dev)
