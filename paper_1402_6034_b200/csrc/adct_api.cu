@@ -162,7 +162,11 @@ void fill_quant_tables(Tables& t, int r, float q) {
       // per weight class (compile-time-r quantiser kernel): dequantiser weight and reciprocal
       t.wc[wclass(k, l)] = (float)((double)q / sqrt(dd_host(k, l)));
       t.cc[wclass(k, l)] = c;
+      const double rq = 1.0 / ((double)q * sqrt(dd_host(k, l)));
+      t.sq[wclass(k, l)] = (float)rq;
+      t.sql[wclass(k, l)] = (float)(rq - (double)(float)rq);
     }
+  t.qscale = (float)(((double)q / 8.0) * ((double)q / 8.0));
 }
 
 template <class K, class P>

@@ -32,6 +32,9 @@ struct Tables {
   float cc[8];   // ZONAL compile-time r: -KF * W per weight class
   float2 w[64];  // ZONAL: (W, W); QUANT: q / sqrt(d_k d_l); INVERSE: per-coef scale — 0 where masked
   float2 c[64];  // ZONAL: (-KF W, -KF W) [masked: 0]; QUANT: (c', c') quantiser reciprocal
+  float sq[8];   // QUANT residual form: 1 / (q sqrt dd) per weight class as hi + lo fp32 pair
+  float sql[8];
+  float qscale;  // QUANT residual form: SSE = (q / 8)^2 * sum of the weighted inverse's squares
 };
 
 struct CompressParams {
@@ -251,6 +254,65 @@ __device__ __forceinline__ float2 compress_resid(const uint32_t (&Y)[8][8], cons
   return f2add(f2add(s01, s23), f2add(s45, s67));
 }
 
+// Residual form of the quantiser error (compile-time r = 64, SSE only; C4's case).  By the same
+// orthogonality, x - x^ = C^T (Z - Z^) C: the kernel inverts the per-coefficient quantisation
+// residual instead of forming x^ and subtracting it from the re-read pixels.  With
+// Z - Z^ = q (Y / (q sqrt dd) - k) = q rho and D's row weights w = (1/sqrt8, 1/sqrt6, 1/2, 1/sqrt6,
+// ...) folded into the butterfly (w_0 factored out, the ratios sqrt2 and 2/sqrt3 as FFMA2 immediates:
+// the same 22 operations per 1-D pass), x - x^ = (q / 8) X'' where X'' is the weighted inverse of
+// rho.  The DC path carries no ratio, so a DC-only residual is exact (pin P18 holds bit for bit).
+constexpr float QW_S2 = 1.41421356f;   // w_2 / w_0 = sqrt 2
+constexpr float QW_RO = 1.15470054f;   // w_1 / w_0 = 2 / sqrt 3
+__device__ __forceinline__ void inv8w(const float2 (&v)[8], float2 (&o)[8]) {
+  const float2 pp = f2add(v[0], v[4]), qq = f2sub(v[0], v[4]);
+  const float2 a0 = f2fma(v[2], f2(QW_S2), pp), a3 = f2fma(v[2], f2(-QW_S2), pp);
+  const float2 a1 = f2fma(v[6], f2(-QW_S2), qq), a2 = f2fma(v[6], f2(QW_S2), qq);
+  const float2 b0 = f2add(f2add(v[1], v[3]), v[5]), b1 = f2sub(f2sub(v[1], v[5]), v[7]);
+  const float2 b2 = f2add(f2sub(v[1], v[3]), v[7]), b3 = f2sub(f2sub(v[5], v[3]), v[7]);
+  o[0] = f2fma(b0, f2(QW_RO), a0);
+  o[7] = f2fma(b0, f2(-QW_RO), a0);
+  o[1] = f2fma(b1, f2(QW_RO), a1);
+  o[6] = f2fma(b1, f2(-QW_RO), a1);
+  o[2] = f2fma(b2, f2(QW_RO), a2);
+  o[5] = f2fma(b2, f2(-QW_RO), a2);
+  o[3] = f2fma(b3, f2(QW_RO), a3);
+  o[4] = f2fma(b3, f2(-QW_RO), a3);
+}
+
+__device__ __forceinline__ float2 compress_quant_resid(const uint32_t (&Y)[8][8], const CompressParams& p) {
+  float2 U[8][8];  // column pass outputs [row][col]
+  static_for<8>([&](auto Lc) {
+    constexpr int L = decltype(Lc)::value;
+    float2 v[8], o[8];
+    static_for<8>([&](auto Kc) {
+      constexpr int K = decltype(Kc)::value, c = wclass(K, L);
+      const float2 y = f2add(biased_pair(Y[K][L]), f2(-KF));                  // Y, exact
+      const float2 t = f2fma(y, f2(p.tab.cc[c]), f2(12582912.0f));           // 1.5 2^23 + k (exact decision, R10)
+      const float2 k = f2add(t, f2(-12582912.0f));
+      // rho = Y / (q sqrt dd) - k with the reciprocal as hi + lo: y hi - k is exact-ish in the fma
+      // (near cancellation), y lo restores the rest — a DC residual that is 0 in exact arithmetic
+      // stays ~1e-13 instead of ~1e-7 (lossless blocks keep SSE ~ 0)
+      v[K] = f2fma(y, f2(p.tab.sql[c]), f2fma(y, f2(p.tab.sq[c]), make_float2(-k.x, -k.y)));
+    });
+    inv8w(v, o);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) U[i][L] = o[i];
+  });
+  float2 acc[8];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) acc[n] = f2(0.f);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    float2 o[8];
+    inv8w(U[i], o);
+#pragma unroll
+    for (int n = 0; n < 8; ++n) acc[n] = f2fma(o[n], o[n], acc[n]);
+  }
+  const float2 s01 = f2add(acc[0], acc[1]), s23 = f2add(acc[2], acc[3]);
+  const float2 s45 = f2add(acc[4], acc[5]), s67 = f2add(acc[6], acc[7]);
+  return f2add(f2add(s01, s23), f2add(s45, s67));
+}
+
 // ------------------------------------------------------------------------------------------
 // Fused compress kernel: every warp owns a TMA ring of ST stages and runs forward + inverse +
 // error on each tile (one warp tile = 16 rows x 256 columns = one block pair per lane).
@@ -274,6 +336,9 @@ constexpr int compress_f16_rows(int R) { return R <= 3 ? 8 : 0; }
 #endif
 constexpr bool compress_grouped(int R) { return ADCT_GROUPED || (R >= 6 && R < ADCT_RESID_FROM); }
 // runtime-mask / quantiser / reconstruction kernels (all 64 coefficients live)
+#ifndef ADCT_MINB_QRES
+#define ADCT_MINB_QRES 2
+#endif
 #ifndef ADCT_MINB_RT
 #define ADCT_MINB_RT 2  // measured: 5-17 % faster than 3 (no spills), profiles/r01_variants_session3.txt
 #endif
@@ -283,14 +348,17 @@ constexpr int compress_minb(int R) {
 }
 
 template <int R, int MODE, int RECON, int ST = compress_stages(R),
-          int MINB = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_minb(R) : ADCT_MINB_RT,
+          int MINB = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_minb(R)
+                     : ((MODE == MODE_QUANT && RECON == REC_NONE && R == 64) ? ADCT_MINB_QRES : ADCT_MINB_RT),
           bool RES = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT && compress_resid_r(R)),
           int F16 = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_f16_rows(R) : 0,
           bool GRP = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_grouped(R) : false>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     k_compress(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CompressParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr double kSseScale = (MODE == MODE_ZONAL) ? 1.0 / 331776.0 : 1.0;  // errors in 576 units (ZONAL)
+  // errors in 576 units (ZONAL); the quantiser's residual form in units of q / 8 (compress_quant_resid)
+  const double kSseScale = (MODE == MODE_ZONAL) ? 1.0 / 331776.0
+                           : ((RECON == REC_NONE && R == 64) ? (double)p.tab.qscale : 1.0);
   // warp index through a shuffle: provably warp-uniform, so ptxas keeps the tile cursor in uniform
   // registers for the TMA (no per-lane R2UR loop)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -312,6 +380,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     if constexpr (RES) {
       compress_fwd<RESID + R, MODE>(tile, lane, Y);
       e2 = compress_resid<R, GRP>(Y, p);
+    } else if constexpr (MODE == MODE_QUANT && RECON == REC_NONE && R == 64) {
+      compress_fwd<64, MODE>(tile, lane, Y);
+      e2 = compress_quant_resid(Y, p);
     } else {
       compress_fwd<R, MODE>(tile, lane, Y);
       e2 = compress_inv<R, MODE, RECON, F16, GRP>(Y, tile, lane, p, img, ty, tx);

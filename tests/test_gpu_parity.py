@@ -255,8 +255,11 @@ def test_compress_quant_vs_oracle(q):
     sse, rec = A.compress_psnr(dev(imgs), 64, q=q, recon="f32")
     assert np.abs(host(rec) - want).max() <= FP_TOL
     check_sse(host(sse), O.sse_per_image(imgs, want), 64 * 64)
+    # SSE only (C4's kernel): the error comes from the inverted quantisation residual
+    # (x - x^ = C^T (Z - Z^) C), not from x - x^ as in the reconstruction kernel — same bar
     sse_only = host(A.compress_psnr(dev(imgs), 64, q=q))
-    assert np.allclose(sse_only, host(sse), rtol=1e-12)
+    check_sse(sse_only, O.sse_per_image(imgs, want), 64 * 64)
+    assert np.allclose(sse_only, host(sse), rtol=SSE_RTOL, atol=1e-6 * 64 * 64)  # floor as check_sse
 
 
 def test_compress_quant_c4_constant_frames_closed_form():
