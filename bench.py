@@ -298,9 +298,10 @@ def main():
     m1.record(stream)
     torch.cuda.synchronize()
     mms = max_over_ranks(m0.elapsed_time(m1) / a.steps, dev)
-    fused = {"what": "adct_compress_psnr_multi: one read + one forward per tile, then for every r the zonal "
-                     "step, inverse and per-pixel error (each r's own arithmetic); NOT the headline, which runs "
-                     "the 8 r-passes independently",
+    fused = {"what": "adct_compress_psnr_multi: one read + one forward per tile; the per-pixel errors "
+                     "576x - R_r of r = 1, 3, ..., 36 by an incremental inverse (each r adds one anti-diagonal "
+                     "band, exact in integers), each r's error squared pixel by pixel; NOT the headline, which "
+                     "runs the 8 r-passes independently",
              "gpix_passes_s": world * n_loc * H * W * len(R_SET) / (mms * 1e-3) / 1e9, "ms": mms,
              "speedup_vs_independent_passes": (ms_step / mms),
              "max_rel_diff_vs_independent_sse": float(((multi_sse - sse[:, lo:hi]).abs() /

@@ -583,6 +583,13 @@ adct_status adct_compress_psnr_multi(const uint8_t* src, int64_t n, int64_t h, i
   fill_zonal_tables(p.tab, 64);  // per-class weights (the compile-time masks need nothing else)
   cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(double) * (size_t)(n * n_r), s);
   if (e != cudaSuccess) return cuda_fail(e);
+#ifndef ADCT_SWEEP_INC
+#define ADCT_SWEEP_INC 1
+#endif
+  if (ADCT_SWEEP_INC) {  // incremental: band b = anti-diagonal b completes r = (b + 1)(b + 2) / 2
+    for (int b = 0; b < 8; ++b) p.rowmap[b] = rowmap[7 - b];  // RSetC5 lists r = 36, 28, ..., 1
+    return launch_compress(sweep_inc_kernel_c5(), 1, map, p, s);
+  }
   return launch_compress(multi_kernel_c5(), 1, map, p, s);
 }
 

@@ -969,8 +969,105 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_MULTI_MINB)
   flush();
 }
 
+// C0's entries at compile time, read off the same 22-addition graph as fwd8 applied to the unit
+// vector e_i (so the sign patterns below can never disagree with the forward butterfly)
+constexpr int c0_entry(int k, int i) {
+  int x[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  x[i] = 1;
+  const int a0 = x[0] + x[7], a1 = x[1] + x[6], a2 = x[2] + x[5], a3 = x[3] + x[4];
+  const int b0 = x[0] - x[7], b1 = x[1] - x[6], b2 = x[2] - x[5], b3 = x[3] - x[4];
+  const int X[8] = {a0 + a3 + a1 + a2, b0 + b1 + b2, a0 - a3, b0 - b2 - b3,
+                    a0 + a3 - a1 - a2, b0 - b1 + b3, a2 - a1, b2 - b1 - b3};
+  return X[k];
+}
+
+// Incremental fused sweep for C5's r set (the triangular numbers 1, 3, ..., 36: each adds one
+// anti-diagonal b = 0..7 of the zig-zag mask).  R_r is linear in the kept coefficients, so with
+// e = 576 x - R, e_{r_b} = e_{r_{b-1}} - dR_b where dR_b = C0^T (W . [band b] . Y) C0.  A band has
+// one coefficient per column, so its column inverse is a sign pattern (T[k][i] V_kl, no adds) and
+// only its row inverse costs butterfly adds; each r's error is still formed pixel by pixel
+// (exactly, in integers < 2^24: tools/exactness_bounds.py, band variant) and squared.
+template <int B, int I, int L> __device__ __forceinline__ auto band_in(const float2 (&V)[64]) {
+  constexpr int k = B - L;
+  if constexpr (k < 0 || k > 7) return Z0{};
+  else if constexpr (c0_entry(k, I) == 0) return Z0{};
+  else if constexpr (c0_entry(k, I) > 0) return FV<false>{V[k * 8 + L]};
+  else return FV<true>{V[k * 8 + L]};
+}
+
+#ifndef ADCT_INC_MINB
+#define ADCT_INC_MINB 2
+#endif
+template <int UNUSED = 0>
+__global__ void __launch_bounds__(WARPS * 32, ADCT_INC_MINB)
+    k_compress_sweep_inc(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CompressParams p) {
+  constexpr int ST = 2, NB = 8;
+  constexpr double kSseScale = 1.0 / 331776.0;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  uint8_t* ring = smem + warp * (ST * TILE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * ST * TILE_BYTES) + warp * ST;
+  const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
+  int cur = -1;
+  double dacc[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) dacc[b] = 0.0;
+  auto flush = [&]() {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const double v = warp_sum(dacc[b]);
+      if (lane == 0 && cur >= 0) atomicAdd(p.sse + (int64_t)p.rowmap[b] * p.sse_stride + cur, v * kSseScale);
+      dacc[b] = 0.0;
+    }
+  };
+  tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
+                      [&](const uint8_t* tile, int img, int ty, int tx) {
+    if (img != cur) {  // warp-uniform
+      flush();
+      cur = img;
+    }
+    uint32_t Y[8][8];
+    compress_fwd<36, MODE_ZONAL>(tile, lane, Y);
+    float2 V[64];
+    static_for<64>([&](auto KLc) {
+      constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
+      if constexpr (k + l < NB) {
+        constexpr int c = wclass(k, l);
+        V[kl] = f2fma(biased_pair(Y[k][l]), f2(p.tab.wc[c]), f2(p.tab.cc[c]));  // W . Y, exact
+      }
+    });
+    float2 acc[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[b] = f2(0.f);
+    static_for<8>([&](auto Ic) {
+      constexpr int I = decltype(Ic)::value;
+      const uint2 wa = lds64_reload(tile + I * TILE_W + lane * 8);
+      const uint2 wb = lds64_reload(tile + (I + 8) * TILE_W + lane * 8);
+      float2 e[8];  // 576 x - R of this output row, R over the bands added so far (none yet)
+      static_for<8>([&](auto Nc) {
+        constexpr int N = decltype(Nc)::value;
+        e[N] = px576b<false>(N < 4 ? wa.x : wa.y, N < 4 ? wb.x : wb.y, N & 3);
+      });
+      static_for<NB>([&](auto Bc) {
+        constexpr int B = decltype(Bc)::value;
+        auto row = inv8(band_in<B, I, 0>(V), band_in<B, I, 1>(V), band_in<B, I, 2>(V), band_in<B, I, 3>(V),
+                        band_in<B, I, 4>(V), band_in<B, I, 5>(V), band_in<B, I, 6>(V), band_in<B, I, 7>(V));
+        static_for<8>([&](auto Nc) {
+          constexpr int N = decltype(Nc)::value;
+          e[N] = rsub(e[N], cuda::std::get<N>(row));  // e_{r_B} = e_{r_{B-1}} - dR_B, exact
+          acc[B] = f2fma(e[N], e[N], acc[B]);
+        });
+      });
+    });
+#pragma unroll
+    for (int b = 0; b < NB; ++b) dacc[b] += (double)acc[b].x + (double)acc[b].y;
+  });
+  flush();
+}
+
 typedef void (*CompressKernel)(CUtensorMap, CompressParams);
 CompressKernel multi_kernel_c5();  // k_compress_multi<RSetC5>, instantiated in multi_r.cu
+CompressKernel sweep_inc_kernel_c5();  // k_compress_sweep_inc, instantiated in multi_r.cu
 // zonal kernels k_compress<r, ZONAL, RECON_NONE>, instantiated in zonal_part*.cu (4 TUs)
 CompressKernel zonal_kernel(int r);
 

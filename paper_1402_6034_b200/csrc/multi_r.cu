@@ -4,4 +4,5 @@
 
 namespace adct {
 CompressKernel multi_kernel_c5() { return &k_compress_multi<RSetC5>; }
+CompressKernel sweep_inc_kernel_c5() { return &k_compress_sweep_inc<0>; }
 }  // namespace adct

@@ -529,7 +529,8 @@ def test_compress_multi_matches_single_passes(order):
     got = host(A.compress_psnr_multi(x, order))
     for k, r in enumerate(order):
         single = host(A.compress_psnr(x, r))
-        assert np.allclose(got[k], single, rtol=1e-12, atol=1e-12), r
+        # the same exact per-pixel errors; the fused sweep sums their squares in another fp32 order
+        assert np.allclose(got[k], single, rtol=SSE_RTOL, atol=1e-12), r
         check_sse(got[k], O.compress_zonal_sse(imgs, r), 48 * 520)
 
 
@@ -538,4 +539,4 @@ def test_compress_multi_c5_full_size_sampled():
     rs = (1, 3, 6, 10, 15, 21, 28, 36)
     got = host(A.compress_psnr_multi(x, rs))
     for k, r in enumerate(rs):
-        assert np.allclose(got[k], host(A.compress_psnr(x, r)), rtol=1e-12), r
+        assert np.allclose(got[k], host(A.compress_psnr(x, r)), rtol=SSE_RTOL), r

@@ -73,3 +73,13 @@ def test_r64_lossless_identity():
 
 def test_exactness_tool_exit_code():
     assert EB.main() == 0
+
+
+def test_band_chain_equals_error_per_r():
+    # k_compress_sweep_inc: after band b the running per-pixel form is 576 x - R_r, r = (b+1)(b+2)/2
+    m, finals = EB.run_band_chain()
+    assert m < 2 ** 24
+    for r, e in finals.items():
+        A_, c = _forms(e)
+        assert np.array_equal(A_, 576 * np.eye(64, dtype=np.int64) - _affine_R(r)), r
+        assert np.all(c == 0)

@@ -112,6 +112,36 @@ def run(r: int, variant: str, bias: int = 0):
     return B.max, out
 
 
+def run_band_chain():
+    """k_compress_sweep_inc: e = 576 x, then for each anti-diagonal band b = 0..7 (r = 1, 3, ..., 36)
+    e -= C0^T (W . [band b] . Y) C0 with the band's column inverse as a sign pattern (one coefficient
+    per column) and its row inverse through inv8.  Returns (max |node|, final error forms per r)."""
+    B = Bound()
+    Y = forms_Y()
+    e = []
+    for i in range(8):
+        row = []
+        for n in range(8):
+            f = np.zeros(65, dtype=np.int64)
+            f[i * 8 + n] = 576
+            row.append(f)
+        e.append(row)
+    finals = {}
+    for band in range(8):
+        for i in range(8):
+            u = []
+            for l in range(8):
+                k = band - l
+                if 0 <= k <= 7 and T[k, i] != 0:
+                    u.append(B.see(T[k, i] * W[k, l] * Y[k, l]))
+                else:
+                    u.append(None)
+            out = inv8(B, u)
+            e[i] = [sub(B, e[i][n], out[n]) for n in range(8)]
+        finals[(band + 1) * (band + 2) // 2] = [row[:] for row in e]
+    return B.max, finals
+
+
 def main():
     worst = 0
     for variant, bias in (("direct", 0), ("direct", DC_BIASES[1]), ("residual", 0)):
@@ -123,6 +153,9 @@ def main():
             worst = max(worst, m)
             row.append(f"{r}:{m}")
         print(variant, f"bias={bias}", " ".join(row))
+    m, _ = run_band_chain()
+    worst = max(worst, m)
+    print("band chain (k_compress_sweep_inc)", m)
     print("max |node| =", worst, "< 2^24 =", 1 << 24, "->", "EXACT" if worst < (1 << 24) else "NOT EXACT")
     return 0 if worst < (1 << 24) else 1
 
