@@ -14,3 +14,10 @@ print(f"# ncu launch list (gpu__time_duration.sum, --clock-control none; cold-ca
 print("# kernel | launches | mean us | share of summed kernel time")
 for k, v in sorted(t.items(), key=lambda kv: -sum(kv[1])):
     print(f"{k} | {len(v)} | {sum(v) / len(v):.1f} | {sum(v) / tot:.4f}")
+# the bench's timed step is the 8 k_compress<r> passes + k_psnr; the other kernels are its secondary
+# lines (fused sweep, Parseval sweep), timed separately
+step = {k: v for k, v in t.items() if "k_compress<" in k or "k_psnr" in k}
+st = sum(sum(v) for v in step.values()) or 1.0
+print("# share within the timed step (k_compress<r> + k_psnr only)")
+for k, v in sorted(step.items(), key=lambda kv: -sum(kv[1])):
+    print(f"{k} | {sum(v) / st:.4f}")
