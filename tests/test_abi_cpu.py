@@ -158,3 +158,18 @@ def test_multi_and_geometry_limits_validation():
     # the device tile cursors are 32-bit: more than 2^30 tiles of 16 x 256 px in one call is rejected
     n_big = (1 << 30) // (2 * 16) + 1                                                     # 512 x 4096 images
     assert lib.adct_compress_psnr(16, n_big, 512, 4096, 4096, 512 * 4096, 10, 0.0, 0, 0, 0, 0, 64, None) == E
+
+
+def test_header_is_plain_c99(tmp_path):
+    """include/adct.h is a C ABI: it compiles as C99 (gcc) with only the CUDA headers on the path."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    src = tmp_path / "h.c"
+    src.write_text('#include "adct.h"\nint main(void) { return (int)ADCT_OK; }\n')
+    r = subprocess.run([gcc, "-std=c99", "-Wall", "-Wextra", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        "-I", "/usr/local/cuda/include", "-c", str(src), "-o", str(tmp_path / "h.o")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
