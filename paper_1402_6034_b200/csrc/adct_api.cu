@@ -344,6 +344,7 @@ adct_status adct_compress_psnr(const uint8_t* src, int64_t n, int64_t h, int64_t
   if ((st = make_u8_map(&map, src, n, h, w, pitch, img_stride))) return st;
   CompressParams p;
   memset(&p, 0, sizeof(p));
+  p.h16magic = 0x64646464u;
   p.geo = make_geo(h, w);
   p.tiles = p.geo.per_img * n;
   p.h = (int)h;
@@ -573,6 +574,7 @@ adct_status adct_compress_psnr_multi(const uint8_t* src, int64_t n, int64_t h, i
   if ((st = make_u8_map(&map, src, n, h, w, pitch, img_stride))) return st;
   CompressParams p;
   memset(&p, 0, sizeof(p));
+  p.h16magic = 0x64646464u;
   p.geo = make_geo(h, w);
   p.tiles = p.geo.per_img * n;
   p.h = (int)h;

@@ -47,6 +47,8 @@ struct CompressParams {
   int64_t recon_pitch, recon_img_stride;
   int64_t sse_stride;  // multi-r kernel: distance between the per-r SSE rows (doubles)
   int rowmap[8];       // multi-r kernel: output row of the k-th r of the compiled set
+  uint32_t h16magic;   // 0x64646464 from the host: a register operand, so the PRMT selector of the
+                       // f16 pixel pairs stays an immediate (no per-PRMT selector materialisation)
   Tables tab;
 };
 
@@ -134,20 +136,38 @@ __device__ __forceinline__ void compress_fwd(const uint8_t* tile, int lane, uint
 // Inverse half: zonal weights / quantiser, inverse with C^T, error against the staged pixels.
 // Returns this lane's partial sum of squared errors (576 units for ZONAL) as an fp32 pair.
 // F16 (compile-time r, zonal, SSE only): the first F16 output rows take their pixels through the
-// f16 magic (one PRMT makes 1024 + x for two pixels, HADD2.F32 widens each on the FMA pipe) and
-// the error in one FFMA2: e = R' - 576 (1024 + x) with R' = R + 589824 injected at the DC weight
-// (T's first row is all ones, so a constant added to V_00 shifts every output by the same
-// amount; |R'| < 2^24 stays exact, tools/exactness_bounds.py).  The other rows keep the f32 magic
-// (two PRMTs per pixel pair on the ALU pipe).  Same instruction count, different ALU/FMA split.
+// f16 magic — one PRMT makes the f16 pair (1024 + x_n, 1024 + x_{n+1}) of two pixels of a block —
+// and each pixel's error is ONE mixed-precision FMA (PTX fma.rn.f32.f16, SASS FHFMA: f16 x f16 +
+// f32 -> f32, full rate on the FMA pipe, the f16 half selected in the operand):
+// e = R' - 576 (1024 + x) with R' = R + 589824 injected at the DC weight (T's first row is all
+// ones, so a constant added to V_00 shifts every output by the same amount; |R'| < 2^24 stays
+// exact, tools/exactness_bounds.py) — the product 576 (1024 + x) is exact inside the FMA.  Per
+// pixel pair: 1 PRMT + 2 FHFMA (vs 2 PRMT + FFMA2 + FADD2 on the f32 route): -1 ALU and -2
+// FMA-pipe cycles.  The other rows keep the f32 magic.
 constexpr float DC_BIAS16 = 589824.0f;  // 576 * 1024
-__device__ __forceinline__ float2 px16(uint32_t wa, uint32_t wb, int pair, int hi) {
-  const uint32_t ha = __byte_perm(wa, 0x64646464u, pair ? 0x4342 : 0x4140);
-  const uint32_t hb = __byte_perm(wb, 0x64646464u, pair ? 0x4342 : 0x4140);
-  const __half2 a = *reinterpret_cast<const __half2*>(&ha), b = *reinterpret_cast<const __half2*>(&hb);
-  return hi ? make_float2(__high2float(a), __high2float(b)) : make_float2(__low2float(a), __low2float(b));
+// 0xE080 = f16(-576), 0x6080 = f16(+576): the sign follows the typed row output (FV<neg> stores -R')
+template <bool HI, bool NEG>
+__device__ __forceinline__ float fhfma576(uint32_t h2, float c) {
+  float d;
+  if constexpr (HI)
+    asm("{.reg .f16 a, b; mov.b32 {_, a}, %1; mov.b16 b, %3; fma.rn.f32.f16 %0, a, b, %2;}"
+        : "=f"(d) : "r"(h2), "f"(c), "n"(NEG ? 0x6080 : 0xE080));
+  else
+    asm("{.reg .f16 a, b; mov.b32 {a, _}, %1; mov.b16 b, %3; fma.rn.f32.f16 %0, a, b, %2;}"
+        : "=f"(d) : "r"(h2), "f"(c), "n"(NEG ? 0x6080 : 0xE080));
+  return d;
 }
-__device__ __forceinline__ float2 err16(float2 F, FV<false> r) { return f2fma(F, f2(-576.f), r.v); }
-__device__ __forceinline__ float2 err16(float2 F, FV<true> r) { return f2fma(F, f2(576.f), r.v); }
+// e for pixel N of row (A, B): R' -/+ 576 (1024 + x), exact
+template <int N, bool NEG>
+__device__ __forceinline__ float2 err_fh(uint32_t ha, uint32_t hb, float2 v) {
+  return make_float2(fhfma576<(N & 1) != 0, NEG>(ha, v.x), fhfma576<(N & 1) != 0, NEG>(hb, v.y));
+}
+template <int N> __device__ __forceinline__ float2 err_fh(uint32_t ha, uint32_t hb, FV<false> r) {
+  return err_fh<N, false>(ha, hb, r.v);
+}
+template <int N> __device__ __forceinline__ float2 err_fh(uint32_t ha, uint32_t hb, FV<true> r) {
+  return err_fh<N, true>(ha, hb, r.v);
+}
 
 template <int R, int MODE, int RECON, int F16 = 0, bool GROUPED = false>
 __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const uint8_t* tile, int lane,
@@ -197,8 +217,11 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
     static_for<8>([&](auto Nc) {
       constexpr int N = decltype(Nc)::value;
       if constexpr (I < F16) {
-        const float2 F = px16(N < 4 ? wa.x : wa.y, N < 4 ? wb.x : wb.y, (N >> 1) & 1, N & 1);
-        const float2 e = err16(F, get<N>(row));  // R' - 576 (1024 + x) = R - 576 x, exact
+        // f16 pairs (1024 + x_n, 1024 + x_{n+1}) of blocks A and B, one PRMT each per two pixels
+        constexpr uint32_t sel = ((N >> 1) & 1) ? 0x4342u : 0x4140u;
+        const uint32_t ha = __byte_perm(N < 4 ? wa.x : wa.y, p.h16magic, sel);
+        const uint32_t hb = __byte_perm(N < 4 ? wb.x : wb.y, p.h16magic, sel);
+        const float2 e = err_fh<N>(ha, hb, get<N>(row));  // R' - 576 (1024 + x) = R - 576 x, exact
         acc[N] = f2fma(e, e, acc[N]);
       } else {
         // ZONAL: 576 x - R, exact integers; QUANT: x - x^ (fp32, irrational weights)
@@ -328,13 +351,14 @@ constexpr int compress_stages(int R) { return 2; }
 #endif
 constexpr int compress_resid_r(int R) { return R >= ADCT_RESID_FROM && R < 64; }
 // output rows per tile that take the f16 error route (ALU -> FMA pipe rebalancing, compress_inv)
-// measured on B200 (profiles/r01_tune_f16_rows.txt): only the ALU-bound small r gain (+1-2 %)
-constexpr int compress_f16_rows(int R) { return R <= 3 ? 8 : 0; }
+// measured on B200 (profiles/r01_tune_fhfma.txt): the FHFMA error route wins for every direct r
+// (r = 1 keeps two rows on the f32 route to balance its ALU-light body)
+constexpr int compress_f16_rows(int R) { return R == 1 ? 6 : 8; }
 // inverse output rows in two register-light groups (inverse2d_grouped)
 #ifndef ADCT_GROUPED
 #define ADCT_GROUPED 0
 #endif
-constexpr bool compress_grouped(int R) { return ADCT_GROUPED || (R >= 6 && R < ADCT_RESID_FROM); }
+constexpr bool compress_grouped(int R) { return ADCT_GROUPED || (R >= 11 && R < ADCT_RESID_FROM); }
 // runtime-mask / quantiser / reconstruction kernels (all 64 coefficients live)
 #ifndef ADCT_MINB_QRES
 #define ADCT_MINB_QRES 2
@@ -344,7 +368,7 @@ constexpr bool compress_grouped(int R) { return ADCT_GROUPED || (R >= 6 && R < A
 #endif
 // measured on B200 (profiles/r01_tune_minb.txt): small r wants occupancy, mid r registers
 constexpr int compress_minb(int R) {
-  return compress_resid_r(R) ? 4 : (R == 1 ? 6 : (R <= 3 ? 5 : (R <= 15 ? 4 : 3)));
+  return compress_resid_r(R) ? 4 : (R == 1 ? 6 : (R <= 3 ? 5 : 4));
 }
 
 template <int R, int MODE, int RECON, int ST = compress_stages(R),

@@ -33,6 +33,7 @@ template <int R, int MIN_CTAS>
 void run(const uint8_t* src, float* out, int sms, int dyn_smem = 0) {
   CompressParams p;
   memset(&p, 0, sizeof(p));
+  p.h16magic = 0x64646464u;
   for (int k = 0; k < 64; ++k) {
     float w = (float)wval(k / 8, k % 8);
     p.tab.wc[wclass(k / 8, k % 8)] = w;

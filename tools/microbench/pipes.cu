@@ -96,6 +96,20 @@ __global__ void __launch_bounds__(256) kern(uint32_t* out, uint32_t seed, unsign
         asm volatile("fma.rn.f32x2 %0, %0, %1, %0;" : "+l"(rr[c]) : "l"(kk));
         asm volatile("mad.lo.s32 %0, %0, %1, %2;" : "+r"(f[c]) : "r"(k1), "r"(k2));
       }
+      // mixed-precision FMA: f16 x f16 + f32 -> f32 (SASS FHFMA)
+      if (OP == 31) asm volatile("{.reg .f16 h; mov.b32 {h, _}, %1; fma.rn.f32.f16 %0, h, h, %0;}" : "+r"(r[c]) : "r"(k1));
+      if (OP == 32) {  // FHFMA + FFMA2 interleaved
+        asm volatile("{.reg .f16 h; mov.b32 {h, _}, %1; fma.rn.f32.f16 %0, h, h, %0;}" : "+r"(r[c]) : "r"(k1));
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %0;" : "+l"(rr[c]) : "l"(kk));
+      }
+      if (OP == 33) {  // FHFMA + PRMT interleaved
+        asm volatile("{.reg .f16 h; mov.b32 {h, _}, %1; fma.rn.f32.f16 %0, h, h, %0;}" : "+r"(r[c]) : "r"(k1));
+        asm volatile("prmt.b32 %0, %0, %1, 0x5140;" : "+r"(f[c]) : "r"(k2));
+      }
+      if (OP == 34) {  // FHFMA + FFMA (scalar) interleaved
+        asm volatile("{.reg .f16 h; mov.b32 {h, _}, %1; fma.rn.f32.f16 %0, h, h, %0;}" : "+r"(r[c]) : "r"(k1));
+        asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+r"(f[c]) : "r"(k1), "r"(k2));
+      }
     }
   }
   unsigned long long t1 = clock64();
@@ -171,5 +185,9 @@ int main() {
   run<28>("dp4a", 1, 1, sms);
   run<29>("prmt+imad", 1, 2, sms);
   run<30>("ffma2+imad", 1, 2, sms);
+  run<31>("fhfma(f16*f16+f32)", 1, 1, sms);
+  run<32>("fhfma+ffma2", 1, 2, sms);
+  run<33>("fhfma+prmt", 1, 2, sms);
+  run<34>("fhfma+ffma", 1, 2, sms);
   return 0;
 }

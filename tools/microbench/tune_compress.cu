@@ -24,6 +24,7 @@ void run(int cshift_max = 4) {
   auto k = k_compress<R, MODE_ZONAL, REC_NONE, ST, MINB, RES, F16, GRP>;
   CompressParams p;
   memset(&p, 0, sizeof(p));
+  p.h16magic = 0x64646464u;
   p.geo.tiles_x = W / TILE_W;
   p.geo.tiles_y = H / TILE_H;
   p.geo.per_img = p.geo.tiles_x * p.geo.tiles_y;
