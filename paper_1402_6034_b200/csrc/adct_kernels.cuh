@@ -1070,7 +1070,11 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INC_MINB)
       float2 e[8];  // 576 x - R of this output row, R over the bands added so far (none yet)
       static_for<8>([&](auto Nc) {
         constexpr int N = decltype(Nc)::value;
-        e[N] = px576b<false>(N < 4 ? wa.x : wa.y, N < 4 ? wb.x : wb.y, N & 3);
+        // 576 (1024 + x) - 589824 = 576 x through the mixed-precision FMA (exact)
+        constexpr uint32_t sel = ((N >> 1) & 1) ? 0x4342u : 0x4140u;
+        const uint32_t ha = __byte_perm(N < 4 ? wa.x : wa.y, p.h16magic, sel);
+        const uint32_t hb = __byte_perm(N < 4 ? wb.x : wb.y, p.h16magic, sel);
+        e[N] = make_float2(fhfma576<(N & 1) != 0, true>(ha, -DC_BIAS16), fhfma576<(N & 1) != 0, true>(hb, -DC_BIAS16));
       });
       static_for<NB>([&](auto Bc) {
         constexpr int B = decltype(Bc)::value;
