@@ -8,6 +8,7 @@ import re, subprocess, sys, glob, os
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ALU = ("IADD3", "LOP3", "PRMT", "SHF", "ISETP", "SEL", "LEA", "I2FP", "PLOP3", "IADD")
 FMA = ("FFMA2", "FADD2", "FMUL2", "IMAD", "HADD2", "FFMA", "FADD", "FMUL", "HFMA2")
+FMA1 = ("FHFMA", "FFMA", "FADD", "FMUL")  # full-rate FMA-pipe ops: 1 cycle (the others 2)
 objs = sys.argv[1:] or sorted(glob.glob(os.path.join(ROOT, "build/obj/zonal_part*.o")))
 res = {}
 for o in objs:
@@ -27,10 +28,11 @@ for o in objs:
         waits = [i for i, op in enumerate(ops) if op == "SYNCS" and i > body[0]]
         seg = ops[body[0]:waits[0]] if waits else ops[body[0]:body[-1]]
         alu = sum(op in ALU for op in seg)
-        fma = sum(op in FMA for op in seg)
-        res[int(m.group(1))] = (len(seg), alu, fma, m.group(2))
+        fma = sum(op in FMA for op in seg) + sum(op in FMA1 for op in seg)
+        fcyc = 2 * sum(op in FMA and op not in FMA1 for op in seg) + sum(op in FMA1 for op in seg)
+        res[int(m.group(1))] = (len(seg), alu, fma, m.group(2), fcyc)
 print(" r  resid  body-instr  ALU  FMA   pipe-cycles  bound(frac of 729)")
 for r in sorted(res):
-    n, a, f, rs = res[r]
-    cyc = max(n, 2 * a, 2 * f)
+    n, a, f, rs, fcyc = res[r]
+    cyc = max(n, 2 * a, fcyc)
     print(f"{r:2d}  {rs}      {n:5d}     {a:4d} {f:4d}   {cyc:5d}        {729 / cyc:.2f}")
