@@ -344,7 +344,7 @@ __device__ __forceinline__ float2 compress_quant_resid(const uint32_t (&Y)[8][8]
 // large r needs the registers.
 // ------------------------------------------------------------------------------------------
 // measured on B200 (profiles/r01_tune_compress.txt): small r wants occupancy, large r registers
-constexpr int compress_stages(int R) { return 2; }
+constexpr int compress_stages(int R) { return (R == 2 || R == 3) ? 3 : 2; }  // r = 2, 3: HBM-side bound
 // residual form from this r on: cheaper once the discarded set is the smaller one
 #ifndef ADCT_RESID_FROM
 #define ADCT_RESID_FROM 24
@@ -368,7 +368,7 @@ constexpr bool compress_grouped(int R) { return ADCT_GROUPED || (R >= 11 && R < 
 #endif
 // measured on B200 (profiles/r01_tune_minb.txt): small r wants occupancy, mid r registers
 constexpr int compress_minb(int R) {
-  return compress_resid_r(R) ? 4 : (R == 1 ? 6 : (R <= 3 ? 5 : 4));
+  return compress_resid_r(R) ? 4 : (R == 1 ? 6 : 4);
 }
 
 template <int R, int MODE, int RECON, int ST = compress_stages(R),
