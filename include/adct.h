@@ -113,6 +113,19 @@ adct_status adct_compress_psnr(const uint8_t* src, int64_t n, int64_t h, int64_t
                                double* sse, adct_stream_t stream);
 
 /*
+ * adct_compress_sse576 — the zonal pass (q = 0) with the EXACT integer error sum:
+ * sse576[i] = sum over image i of (576 x - R)^2, R = C0^T (W . M_r . Y) C0 (576 X^ = R),
+ * every term an exact integer squared and summed in 64-bit integers (bit-exact; no fp rounding).
+ * Same forward / mask / inverse as adct_compress_psnr with q = 0 (the runtime-mask kernel).
+ *   sse576  device uint64_t[n], OVERWRITTEN.      sse  optional device double[n]: sse576 / 576^2.
+ *   EINVAL additionally when h * w > 2^27 (the per-image sum must stay below 2^64: |576 x - R| <=
+ *   329205).  A validation path: slower than adct_compress_psnr (64-bit multiply-adds per pixel).
+ */
+adct_status adct_compress_sse576(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                                 int64_t img_stride, int r, uint64_t* sse576, double* sse,
+                                 adct_stream_t stream);
+
+/*
  * adct_psnr — PSNR = 10 log10(255^2 * pixels / sse[i]), +inf when sse[i] == 0.
  *   sse, psnr  device double[count]; pixels = h * w of each image (> 0).
  */

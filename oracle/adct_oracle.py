@@ -32,7 +32,7 @@ __all__ = [
     "zigzag_order", "zigzag_index", "zonal_mask", "to_blocks", "from_blocks",
     "forward_int", "forward_scaled", "inverse", "reconstruct_zonal", "reconstruct_zonal_exact",
     "quantize_exact", "reconstruct_quant", "sse_per_image", "psnr", "mean_psnr",
-    "compress_zonal_sse", "compress_quant_sse", "round_u8", "uqi", "ape",
+    "compress_zonal_sse", "compress_zonal_sse576", "compress_quant_sse", "round_u8", "uqi", "ape",
 ]
 
 
@@ -318,6 +318,17 @@ def compress_zonal_sse(img: np.ndarray, r: int, T: np.ndarray | None = None) -> 
     if img.ndim == 2:
         img = img[None]
     return sse_per_image(img, reconstruct_zonal(img, r, T))
+
+
+def compress_zonal_sse576(img: np.ndarray, r: int) -> np.ndarray:
+    """Exact integer twin of compress_zonal_sse: per-image sum of (576 x - R)^2 (int64), where
+    576 A_hat = R = C0^T (W . M_r . Y) C0 (reconstruct_zonal_exact), so
+    SSE = sse576 / 576^2 exactly (P:496-497 on the unrounded reconstruction, R3)."""
+    img = np.asarray(img)
+    if img.ndim == 2:
+        img = img[None]
+    e = 576 * img.astype(np.int64) - reconstruct_zonal_exact(img, r)
+    return (e * e).reshape(img.shape[0], -1).sum(axis=1)
 
 
 def compress_quant_sse(img: np.ndarray, q: float) -> np.ndarray:

@@ -29,6 +29,7 @@ SIGNATURES = {
     "adct_compress_psnr_host": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _i32, _f32, _vp, _i64,
                                        _vp, _vp, _vp]),
     "adct_compress_psnr_multi": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _i32, _vp, _vp]),
+    "adct_compress_sse576": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _vp]),
     "adct_quant_reciprocals": (_i32, [_f32, _vp]),
     "adct_compress_psnr_dense": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _i32, _vp, _vp, _i64, _i64,
                                         _vp, _vp]),
@@ -271,6 +272,28 @@ def compress_psnr_multi(x, r_list, sse=None, stream=None):
     _check(load().adct_compress_psnr_multi(p, n, h, w, pitch, istr, rl, nr, sse.data_ptr(), _stream(stream)),
            "adct_compress_psnr_multi")
     return sse
+
+
+def compress_sse576(x, r: int, sse576=None, sse=None, stream=None):
+    """adct_compress_sse576: exact per-image sum of (576 x - R)^2 as int64 [n] (zonal, q = 0).
+
+    Bit-exact integer result (the fused kernel's fp32 accumulation is replaced by 64-bit integer
+    adds).  If ``sse`` (float64 [n]) is given it also receives sse576 / 576^2.  Returns sse576
+    (values < 2^63 for every accepted size, so the int64 view is exact)."""
+    torch = _torch()
+    p, n, h, w, pitch, istr = _plane(x, 1)
+    if sse576 is None:
+        sse576 = torch.empty(n, dtype=torch.int64, device=x.device)
+    if sse576.dtype != torch.int64 or not sse576.is_contiguous() or sse576.numel() != n:
+        raise ValueError("sse576 must be a contiguous int64 tensor of n entries")
+    sp = None
+    if sse is not None:
+        if sse.dtype != torch.float64 or not sse.is_contiguous() or sse.numel() != n:
+            raise ValueError("sse must be a contiguous float64 tensor of n entries")
+        sp = sse.data_ptr()
+    _check(load().adct_compress_sse576(p, n, h, w, pitch, istr, int(r), sse576.data_ptr(), sp, _stream(stream)),
+           "adct_compress_sse576")
+    return sse576
 
 
 def psnr(sse, pixels: int, out=None, stream=None):

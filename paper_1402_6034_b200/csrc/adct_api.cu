@@ -372,6 +372,37 @@ adct_status adct_compress_psnr(const uint8_t* src, int64_t n, int64_t h, int64_t
   return launch_compress(k_compress<RT, MODE_ZONAL, REC_U8>, RT, map, p, s);
 }
 
+adct_status adct_compress_sse576(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                                 int64_t img_stride, int r, uint64_t* sse576, double* sse,
+                                 adct_stream_t stream) {
+  adct_status st = check_geom(n, h, w);
+  if (st) return st;
+  if (r < 1 || r > 64 || !sse576) return ADCT_EINVAL;
+  if (h * w > (int64_t(1) << 27)) return ADCT_EINVAL;  // per-image sum < 2^64 (|576 x - R| <= 329205)
+  if ((st = check_plane(src, h, w, pitch, img_stride))) return st;
+  if (((uintptr_t)sse576 & 7u) || ((uintptr_t)sse & 7u)) return ADCT_EALIGN;
+  CUtensorMap map;
+  if ((st = make_u8_map(&map, src, n, h, w, pitch, img_stride))) return st;
+  CompressParams p;
+  memset(&p, 0, sizeof(p));
+  p.geo = make_geo(h, w);
+  p.tiles = p.geo.per_img * n;
+  p.h = (int)h;
+  p.w = (int)w;
+  p.sse576 = reinterpret_cast<unsigned long long*>(sse576);
+  fill_zonal_tables(p.tab, r);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(sse576, 0, sizeof(uint64_t) * (size_t)n, s);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if ((st = launch_compress(k_compress_exact<2>, RT, map, p, s))) return st;
+  if (!sse) return ADCT_OK;
+  const int64_t blocks = (n + 255) / 256;
+  k_sse576_to_f64<0><<<(unsigned)(blocks < 1024 ? blocks : 1024), 256, 0, s>>>(p.sse576, sse, n);
+  ++g_launches;
+  e = cudaGetLastError();
+  return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
+}
+
 // The library's own matrices (independent of the CPU oracle): exact DCT-II from cos, C0 = [2C]
 // with Matlab rounding, S from diag(C0 C0^T)^(-1/2), SDCT = sign(C)/(2 sqrt 2), coarse = C0 / 2.
 static void build_matrix(adct_transform_t t, double* M) {

@@ -21,7 +21,7 @@ def header_functions():
 def test_library_exports_every_declared_symbol():
     lib = A.load()
     names = header_functions()
-    assert len(names) == 16
+    assert len(names) == 17
     for name in names:
         assert hasattr(lib, name), name
         assert name in _lib.SIGNATURES, name
@@ -158,6 +158,20 @@ def test_multi_and_geometry_limits_validation():
     # the device tile cursors are 32-bit: more than 2^30 tiles of 16 x 256 px in one call is rejected
     n_big = (1 << 30) // (2 * 16) + 1                                                     # 512 x 4096 images
     assert lib.adct_compress_psnr(16, n_big, 512, 4096, 4096, 512 * 4096, 10, 0.0, 0, 0, 0, 0, 64, None) == E
+
+
+def test_sse576_validation():
+    lib = A.load()
+    E, AL = _lib.ADCT_EINVAL, _lib.ADCT_EALIGN
+    assert lib.adct_compress_sse576(16, 1, 8, 16, 16, 128, 0, 64, None, None) == E     # r = 0
+    assert lib.adct_compress_sse576(16, 1, 8, 16, 16, 128, 65, 64, None, None) == E    # r = 65
+    assert lib.adct_compress_sse576(16, 1, 8, 16, 16, 128, 10, None, None, None) == E  # no sse576
+    assert lib.adct_compress_sse576(16, 1, 8, 16, 16, 128, 10, 68, None, None) == AL   # misaligned
+    assert lib.adct_compress_sse576(16, 1, 8, 16, 16, 128, 10, 64, 68, None) == AL     # misaligned sse
+    assert lib.adct_compress_sse576(16, 1, 7, 16, 16, 128, 10, 64, None, None) == E    # h % 8
+    # the per-image u64 sum is bounded by 329205^2 h w: h w > 2^27 is rejected
+    h, w = 8192, 16392
+    assert lib.adct_compress_sse576(16, 1, h, w, w, h * w, 10, 64, None, None) == E
 
 
 def test_header_is_plain_c99(tmp_path):

@@ -173,6 +173,32 @@ def test_compress_c2_full_mean_psnr():
         assert abs(O.mean_psnr(sse, 512 * 512) - O.mean_psnr(want, 512 * 512)) <= PSNR_TOL
 
 
+@pytest.mark.parametrize("h,w", [(64, 96), (40, 264), (24, 520)])
+def test_compress_sse576_bit_exact(h, w):
+    """adct_compress_sse576: sum (576 x - R)^2 per image, bit-exact against the oracle's int64,
+    every r, ragged tiles, plus the extreme images (all 0 / all 255 / checkerboards)."""
+    imgs = np.concatenate([rng.integers(0, 256, (3, h, w), dtype=np.uint8),
+                           S.corpus_c2(2, h, w),
+                           np.zeros((1, h, w), np.uint8), np.full((1, h, w), 255, np.uint8),
+                           (255 * ((np.arange(h)[:, None] + np.arange(w)[None]) % 2)).astype(np.uint8)[None]])
+    x = dev(imgs)
+    for r in range(1, 65):
+        got = host(A.compress_sse576(x, r))
+        assert np.array_equal(got, O.compress_zonal_sse576(imgs, r)), r
+        if r in (1, 10, 36):  # and the fp32-accumulated fused path agrees within its stated bound
+            check_sse(host(A.compress_psnr(x, r)), got / 576.0 ** 2, h * w)
+
+
+def test_compress_sse576_c1_and_f64_output():
+    img = S.image_c1(0)
+    x = dev(img)
+    sse = torch.empty(1, dtype=torch.float64, device="cuda")
+    got = host(A.compress_sse576(x, 10, sse=sse))
+    want = O.compress_zonal_sse576(img, 10)
+    assert np.array_equal(got, want)
+    assert host(sse)[0] == float(want[0]) / 331776.0
+
+
 @pytest.mark.parametrize("r", [1, 3, 6, 10, 15, 21, 28, 36, 7, 50])
 def test_compress_recon_f32_and_u8(r):
     imgs = np.concatenate([S.corpus_c2(3, 64, 96),
@@ -244,6 +270,18 @@ def test_compress_c5_sampled_images_vs_oracle():
     imgs = host(x)
     for r in (1, 10, 36):
         check_sse(host(A.compress_psnr(x, r)), O.compress_zonal_sse(imgs, r), 4096 * 4096)
+
+
+def test_compress_sse576_c5_images_bit_exact():
+    """Three full-size C5 images (one per kind): the exact integer error sum, bit for bit, and
+    the headline kernels' fp32-accumulated SSE against it (the accumulation bound SSE_RTOL)."""
+    x = S.device_mixed(3, 4096, 4096, seed=0)
+    imgs = host(x)
+    for r in (1, 15, 36):
+        exact = host(A.compress_sse576(x, r))
+        assert np.array_equal(exact, O.compress_zonal_sse576(imgs, r)), r
+        fused = host(A.compress_psnr(x, r))
+        assert np.all(np.abs(fused - exact / 576.0 ** 2) <= SSE_RTOL * exact / 576.0 ** 2)
 
 
 # ------------------------------------------------------------------ fused compress (quantiser)

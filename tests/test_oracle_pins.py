@@ -213,13 +213,31 @@ def test_P9_parseval_exact_integer_identity():
     x = img.astype(np.int64)
     for r in (1, 5, 10, 17, 36, 63, 64):
         R = O.reconstruct_zonal_exact(img, r)
-        sse576 = ((576 * x - R) ** 2).reshape(3, -1).sum(1)
+        sse576 = O.compress_zonal_sse576(img, r)
         kept = (W * O.zonal_mask(r) * Y * Y).reshape(3, -1).sum(1)
         assert np.array_equal(sse576, 576 * (576 * (x * x).reshape(3, -1).sum(1) - kept))
         sse = O.compress_zonal_sse(img, r)
         assert np.allclose(sse, sse576 / 576.0 ** 2, rtol=1e-10, atol=1e-9)
         rec = O.reconstruct_zonal(img, r)
         assert np.abs(rec - R / 576.0).max() < 1e-10
+
+
+def test_P9b_sse576_dc_only_closed_form_and_lossless():
+    # r = 1 keeps only the DC: every pixel of a block reconstructs to the block mean, so
+    # 576 x - R = 576 x - 9 S = 9 (64 x - S) (S = block sum; W_00 = 576 / 64 = 9) and
+    # sse576 = 81 sum (64 x - S)^2 — brute force over the blocks, no transform involved
+    img = S.corpus_c2(2, 32, 48)
+    want = []
+    for im in img.astype(np.int64):
+        tot = 0
+        for by in range(0, 32, 8):
+            for bx in range(0, 48, 8):
+                b = im[by:by + 8, bx:bx + 8]
+                tot += int(81 * ((64 * b - b.sum()) ** 2).sum())
+        want.append(tot)
+    assert O.compress_zonal_sse576(img, 1).tolist() == want
+    assert np.all(O.compress_zonal_sse576(img, 64) == 0)          # P8: r = 64 is lossless
+    assert O.compress_zonal_sse576(img, 10).dtype == np.int64
 
 
 def test_P10_sse_monotone_in_r():

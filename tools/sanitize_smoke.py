@@ -26,6 +26,7 @@ def main():
         for r in (1, 3, 6, 10, 15, 21, 28, 36, 50, 64):
             A.compress_psnr(x, r)
         A.compress_psnr(x, 10, recon="f32")
+        A.compress_sse576(x, 10)
         A.compress_psnr(x, 36, recon="u8")
         A.compress_psnr(x, 64, q=16.0)
         A.compress_psnr(x, 20, q=5.0, recon="u8")

@@ -55,6 +55,8 @@ def main():
         add(f"zonal r={r} SSE only (compile-time r)", best_ms(lambda: A.compress_psnr(x, r, sse=sse)), 1)
         add(f"zonal r={r} + f32 recon", best_ms(lambda: A.compress_psnr(x, r, sse=sse, recon="f32", recon_out=rec_f)), 5)
         add(f"zonal r={r} + u8 recon", best_ms(lambda: A.compress_psnr(x, r, sse=sse, recon="u8", recon_out=rec_u)), 2)
+    s576 = torch.empty(32, dtype=torch.int64, device="cuda")
+    add("zonal r=10 exact u64 SSE (adct_compress_sse576)", best_ms(lambda: A.compress_sse576(x, 10, sse576=s576)), 1)
     add("quant q=16 SSE only", best_ms(lambda: A.compress_psnr(x, 64, q=16.0, sse=sse)), 1)
     add("quant q=16 + u8 recon", best_ms(lambda: A.compress_psnr(x, 64, q=16.0, sse=sse, recon="u8", recon_out=rec_u)), 2)
     add("forward int16 (r=64)", best_ms(lambda: A.forward(x, out=coef)), 3)
