@@ -181,7 +181,7 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
     if constexpr (kept(RF, k, l)) {
       if constexpr (MODE == MODE_ZONAL && RF < RT) {
         // scalar weight / offset broadcast to both lanes from 12 loop-invariant class constants:
-        // an FFMA2 that reads three distinct register pairs issues at 1/3 rate on B200
+        // an FFMA2 that reads three distinct register pairs issues at 2/3 rate on B200 (tools/microbench/ffma2_forms.cu)
         constexpr int c = wclass(k, l);
         const float cc = (F16 > 0 && kl == 0) ? p.tab.cc[c] + DC_BIAS16 : p.tab.cc[c];
         V[kl] = f2fma(biased_pair(Y[k][l]), f2(p.tab.wc[c]), f2(cc));  // W . M . Y (+ bias), exact
