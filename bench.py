@@ -375,6 +375,31 @@ def main():
                     "ms": fms, "gb_s": 3 * px / (fms * 1e-3) / 1e9, "frac": 3 * px / (fms * 1e-3) / 1e9 / peak}
         del xs, out
 
+    # ---- secondary (N = 1): C4 quantiser (240 x 4320x7680 video frames, q = 16, SSE + PSNR), 1 B/px
+    quant_c4 = None
+    if world == 1 and not a.no_fwd_only:
+        nf = 240
+        v = S.device_video(nf, 4320, 7680, seed=a.seed, device=dev)
+        sse4 = torch.empty(nf, dtype=torch.float64, device=dev)
+        ps4 = torch.empty(nf, dtype=torch.float64, device=dev)
+        for _ in range(3):
+            A.compress_psnr(v, 64, q=16.0, sse=sse4)
+        torch.cuda.synchronize()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        for _ in range(5):
+            A.compress_psnr(v, 64, q=16.0, sse=sse4)
+            A.psnr(sse4, 4320 * 7680, out=ps4)
+        q1.record(stream)
+        torch.cuda.synchronize()
+        qms = q0.elapsed_time(q1) / 5
+        px = nf * 4320 * 7680
+        quant_c4 = {"workload": "C4: 240 x 4320x7680 video frames, fwd + D-scaled quantiser q=16 + inverse + "
+                                "per-frame PSNR (k_compress<64, QUANT> residual form)",
+                    "gpix_s": px / (qms * 1e-3) / 1e9, "ms": qms, "gb_s": px / (qms * 1e-3) / 1e9,
+                    "frac": px / (qms * 1e-3) / 1e9 / peak, "mean_psnr_db": float(ps4.mean().item())}
+        del v, sse4, ps4
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cpu = cpu_oracle_sample(a.seed)
@@ -388,7 +413,7 @@ def main():
                            "parallelism": f"dp{world} (images sharded; one NCCL all-reduce of per-image SSE)",
                            "l2": "inputs 64 GiB >> 126 MB L2 (no flush needed)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clocks, "issue_roofline": issue, "fwd_only_c3": fwd_only, "parseval_sweep_f3": sweep,
+                "clocks": clocks, "issue_roofline": issue, "fwd_only_c3": fwd_only, "quant_c4": quant_c4, "parseval_sweep_f3": sweep,
                 "fused_multi_r_c5": fused,
                 "mean_psnr_db": {str(r): float(np.mean(ps[k])) for k, r in enumerate(R_SET)}}
         print(json.dumps(line), flush=True)
