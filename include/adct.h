@@ -118,8 +118,9 @@ adct_status adct_compress_psnr(const uint8_t* src, int64_t n, int64_t h, int64_t
  * every term an exact integer squared and summed in 64-bit integers (bit-exact; no fp rounding).
  * Same forward / mask / inverse as adct_compress_psnr with q = 0 (the runtime-mask kernel).
  *   sse576  device uint64_t[n], OVERWRITTEN.      sse  optional device double[n]: sse576 / 576^2.
- *   EINVAL additionally when h * w > 2^27 (the per-image sum must stay below 2^64: |576 x - R| <=
- *   329205).  A validation path: slower than adct_compress_psnr (64-bit multiply-adds per pixel).
+ *   EINVAL additionally when h * w > 2^26 (the per-image sum must stay below 2^63, so the result is
+ *   also exact as int64: |576 x - R| <= 329205).  A validation path: slower than
+ *   adct_compress_psnr (64-bit multiply-adds per pixel).
  */
 adct_status adct_compress_sse576(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
                                  int64_t img_stride, int r, uint64_t* sse576, double* sse,

@@ -378,7 +378,7 @@ adct_status adct_compress_sse576(const uint8_t* src, int64_t n, int64_t h, int64
   adct_status st = check_geom(n, h, w);
   if (st) return st;
   if (r < 1 || r > 64 || !sse576) return ADCT_EINVAL;
-  if (h * w > (int64_t(1) << 27)) return ADCT_EINVAL;  // per-image sum < 2^64 (|576 x - R| <= 329205)
+  if (h * w > (int64_t(1) << 26)) return ADCT_EINVAL;  // per-image sum < 2^63 (|576 x - R| <= 329205)
   if ((st = check_plane(src, h, w, pitch, img_stride))) return st;
   if (((uintptr_t)sse576 & 7u) || ((uintptr_t)sse & 7u)) return ADCT_EALIGN;
   CUtensorMap map;

@@ -423,7 +423,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
 // as k_compress<RT, ZONAL>, but every per-pixel error e = 576 x - R (an exact integer, |e| < 2^19,
 // tools/exactness_bounds.py) is squared and summed in 64-bit integers, so the per-image result
 // sum (576 x - R)^2 is bit-exact (no fp32 accumulation).  |e| <= 329205, so
-// e^2 < 1.09e11 and the per-image sum fits u64 for h w <= 2^27 (checked by the host entry).
+// e^2 < 1.09e11 and the per-image sum stays below 2^63 (int64-safe) for h w <= 2^26 (host check).
 // A parity / validation kernel, not the headline: 64-bit multiply-adds instead of FFMA2.
 // ------------------------------------------------------------------------------------------
 __device__ __forceinline__ unsigned long long sq_exact(float e) {

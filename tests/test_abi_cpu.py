@@ -169,8 +169,8 @@ def test_sse576_validation():
     assert lib.adct_compress_sse576(16, 1, 8, 16, 16, 128, 10, 68, None, None) == AL   # misaligned
     assert lib.adct_compress_sse576(16, 1, 8, 16, 16, 128, 10, 64, 68, None) == AL     # misaligned sse
     assert lib.adct_compress_sse576(16, 1, 7, 16, 16, 128, 10, 64, None, None) == E    # h % 8
-    # the per-image u64 sum is bounded by 329205^2 h w: h w > 2^27 is rejected
-    h, w = 8192, 16392
+    # the per-image sum is bounded by 329205^2 h w < 2^63 only for h w <= 2^26: larger is rejected
+    h, w = 8192, 8200
     assert lib.adct_compress_sse576(16, 1, h, w, w, h * w, 10, 64, None, None) == E
 
 
