@@ -213,7 +213,8 @@ def test_compress_recon_f32_and_u8(r):
     assert np.allclose(host(sse2), host(sse), rtol=1e-12)
 
 
-@pytest.mark.parametrize("h,w", [(8, 8), (8, 16), (24, 504), (40, 264), (264, 8), (16, 520)])
+@pytest.mark.parametrize("h,w", [(8, 8), (8, 16), (24, 504), (40, 264), (264, 8), (16, 520),
+                                 (8, 131080), (65544, 8)])
 def test_compress_ragged_shapes(h, w):
     imgs = rng.integers(0, 256, (5, h, w), dtype=np.uint8)
     for r in (1, 10, 36, 64):
@@ -457,6 +458,27 @@ def test_diag_energy_bit_exact_and_sweep_sse():
             check_sse(fused, sse[k], 64 * 96)
         else:
             assert np.all(sse[k] == 0) and np.all(fused < 1e-6)
+
+
+@pytest.mark.parametrize("h,w", [(8, 131080), (65544, 8)])
+def test_extreme_aspect_ratios_every_entry(h, w):
+    """One block row 131080 px wide / one block column 65544 px tall (many tile columns / rows, a
+    ragged last tile): forward (bit-exact), inverse (u8 exact), fused multi-r, exact SSE, Parseval."""
+    imgs = rng.integers(0, 256, (2, h, w), dtype=np.uint8)
+    x = dev(imgs)
+    Y = host(A.forward(x)).astype(np.int64)
+    Yo = O.forward_int(imgs)
+    assert np.array_equal(Y, Yo)
+    u8 = host(A.inverse(dev(Yo.astype(np.int16)), r=10, out="u8"))
+    assert np.array_equal(u8, O.round_u8(O.reconstruct_zonal_exact(imgs, 10) / 576.0))
+    rs = (1, 3, 6, 10, 15, 21, 28, 36)
+    multi = host(A.compress_psnr_multi(x, rs))
+    E = host(A.diag_energy(x))
+    assert np.array_equal(E[:, :15].astype(np.int64), oracle_diag_energy(imgs))
+    for k, r in enumerate(rs):
+        exact = O.compress_zonal_sse576(imgs, r)
+        assert np.array_equal(host(A.compress_sse576(x, r)), exact), r
+        check_sse(multi[k], exact / 576.0 ** 2, h * w)
 
 
 def test_diag_energy_c5_full_size_sampled():
