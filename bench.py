@@ -147,14 +147,14 @@ class ClockSampler:
 def _oracle_image_task(args):
     """Pool worker: one C5 image (generated untimed) through the oracle at all 8 r.
     Returns (pixels, t_start, t_end) in host wall-clock seconds."""
-    seed, kind = args
+    seed, kind, h, w = args
     import oracle as O
     from synth import images as S
-    img = S.image_kind(seed, kind, H, W, rect_scale=8)[None]
+    img = S.image_kind(seed, kind, h, w, rect_scale=8)[None]
     t0 = time.time()
     for r in R_SET:
         O.compress_zonal_sse(img, r)
-    return len(R_SET) * H * W, t0, time.time()
+    return len(R_SET) * h * w, t0, time.time()
 
 
 def oracle_pool(workers: int):
@@ -163,10 +163,10 @@ def oracle_pool(workers: int):
     return mp.get_context("spawn").Pool(workers)
 
 
-def oracle_pool_step(pool, workers: int, seed: int):
+def oracle_pool_step(pool, workers: int, seed: int, h: int = H, w: int = W):
     """One parallel round: `workers` C5 images x 8 r, one per worker; throughput over the span from
     the first worker's start to the last worker's end (generation excluded, stagger included)."""
-    res = pool.map(_oracle_image_task, [(seed * 7 + k, k % 3) for k in range(workers)], chunksize=1)
+    res = pool.map(_oracle_image_task, [(seed * 7 + k, k % 3, h, w) for k in range(workers)], chunksize=1)
     px = sum(r[0] for r in res)
     wall = max(r[2] for r in res) - min(r[1] for r in res)
     return px, wall
