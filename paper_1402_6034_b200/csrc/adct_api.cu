@@ -199,6 +199,34 @@ adct_status launch_tma_kernel(K kern, const CUtensorMap& map, const P& params_in
 
 
 
+// Forward to an int16 plane with TMA bulk stores (k_forward_i16_tma): two tensor maps.
+adct_status launch_forward_tma(const CUtensorMap& map, const CUtensorMap& omap, const ForwardParams& params_in,
+                               cudaStream_t stream) {
+  ForwardParams params = params_in;
+  auto kern = k_forward_i16_tma<0>;
+  const int smem = fwdt_smem_bytes();
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return cuda_fail(e);
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, smem);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (occ < 1) occ = 1;
+  int64_t grid = (int64_t)sms * occ;
+  int cshift = 4;
+  while (cshift > 0 && (params.tiles >> cshift) < 2 * grid * WARPS) --cshift;
+  params.cshift = cshift;
+  const int64_t chunks = (params.tiles + (int64_t(1) << cshift) - 1) >> cshift;
+  const int64_t need = (chunks + WARPS - 1) / WARPS;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, WARPS * 32, smem, stream>>>(map, omap, params);
+  ++g_launches;
+  e = cudaGetLastError();
+  return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
+}
+
 // Compress launch: ring depth from the kernel's per-r configuration.
 adct_status launch_compress(CompressKernel kern, int RF, const CUtensorMap& map, const CompressParams& p,
                             cudaStream_t stream) {
@@ -260,7 +288,17 @@ adct_status adct_forward(const uint8_t* src, int64_t n, int64_t h, int64_t w, in
       p.sc[k * 8 + l] = (zz_host(k, l) < r) ? (float)(1.0 / sqrt(dd_host(k, l))) : 0.f;
   cudaStream_t s = (cudaStream_t)stream;
   switch (coef_t) {
-    case ADCT_COEF_I16: return launch_tma_kernel(k_forward<OUT_I16>, map, p, p.tiles, s, FWD_ST);
+    case ADCT_COEF_I16: {
+#ifndef ADCT_FWD_TMA_STORE
+#define ADCT_FWD_TMA_STORE 1
+#endif
+      if (ADCT_FWD_TMA_STORE) {
+        CUtensorMap omap;
+        if ((st = make_i16_map(&omap, coef, n, h, w, coef_pitch, coef_img_stride))) return st;
+        return launch_forward_tma(map, omap, p, s);
+      }
+      return launch_tma_kernel(k_forward<OUT_I16>, map, p, p.tiles, s, FWD_ST);
+    }
     case ADCT_COEF_I32: return launch_tma_kernel(k_forward<OUT_I32>, map, p, p.tiles, s, FWD_ST);
     default: return launch_tma_kernel(k_forward<OUT_F32>, map, p, p.tiles, s, FWD_ST);
   }

@@ -568,6 +568,79 @@ __global__ void __launch_bounds__(WARPS * 32, FWD_MINB)
 }
 
 // ------------------------------------------------------------------------------------------
+// Forward to an int16 plane with TMA bulk-tensor stores: each warp writes its 16 x 256 tile of
+// coefficients (8 KiB) into a warp-private shared-memory staging buffer and one elected lane
+// stores it with cp.async.bulk.tensor (edges clipped by the tensor map), instead of 16 STG.128
+// per lane.  NSTG staging buffers per warp: the buffer is rewritten only after the bulk store
+// that read it NSTG tiles ago has finished reading (cp.async.bulk.wait_group.read).
+// ------------------------------------------------------------------------------------------
+#ifndef ADCT_FWDT_ST
+#define ADCT_FWDT_ST 2
+#endif
+#ifndef ADCT_FWDT_NSTG
+#define ADCT_FWDT_NSTG 2
+#endif
+#ifndef ADCT_FWDT_MINB
+#define ADCT_FWDT_MINB 2
+#endif
+constexpr int FWDT_ST = ADCT_FWDT_ST, FWDT_NSTG = ADCT_FWDT_NSTG;
+constexpr int FWDT_BAR_BYTES = 128;  // mbarriers, padded so the staging buffers stay 128-B aligned
+constexpr int fwdt_smem_bytes() { return WARPS * FWDT_ST * TILE_BYTES + FWDT_BAR_BYTES + WARPS * FWDT_NSTG * 2 * TILE_BYTES; }
+__device__ __forceinline__ void bulk_store_3d(const CUtensorMap* map, uint32_t src, int x, int y, int z) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)), "r"(src), "r"(x), "r"(y), "r"(z)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N> __device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int UNUSED = 0>
+__global__ void __launch_bounds__(WARPS * 32, ADCT_FWDT_MINB)
+    k_forward_i16_tma(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
+                      const __grid_constant__ ForwardParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  static_assert(WARPS * FWDT_ST * 8 <= FWDT_BAR_BYTES, "mbarrier area");
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  uint8_t* ring = smem + warp * (FWDT_ST * TILE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * FWDT_ST * TILE_BYTES) + warp * FWDT_ST;
+  uint8_t* stg = smem + WARPS * FWDT_ST * TILE_BYTES + FWDT_BAR_BYTES + warp * (FWDT_NSTG * 2 * TILE_BYTES);
+  const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
+  int sidx = 0;
+  tma_ring_loop_u<FWDT_ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
+                           [&](const uint8_t* tile, int img, int ty, int tx) {
+    uint8_t* buf = stg + sidx * (2 * TILE_BYTES);
+    uint32_t P[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      pack_rows(lds64(tile + i * TILE_W + lane * 8), lds64(tile + (i + 8) * TILE_W + lane * 8), P[i]);
+    uint32_t Y[8][8];
+    fwd2d<0x8000u, 64>(P, Y);
+    if (lane == 0) bulk_wait_read<FWDT_NSTG - 1>();  // the store that last read `buf` is done reading
+    __syncwarp();
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        uint32_t o[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          o[m] = b ? __byte_perm(Y[k][2 * m], Y[k][2 * m + 1], 0x7632)
+                   : (__byte_perm(Y[k][2 * m], Y[k][2 * m + 1], 0x5410) ^ 0x80008000u);
+          if (p.masked) o[m] &= p.m16[k * 4 + m];
+        }
+        *reinterpret_cast<uint4*>(buf + (b * 8 + k) * (2 * TILE_W) + lane * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> bulk copy
+    __syncwarp();
+    if (lane == 0) bulk_store_3d(&omap, smem_u32(buf), tx * TILE_W, ty * TILE_H, img);
+    if constexpr (FWDT_NSTG > 1) sidx = (sidx + 1 == FWDT_NSTG) ? 0 : sidx + 1;
+  });
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// ------------------------------------------------------------------------------------------
 // Inverse only: coefficient plane -> reconstruction (direct vectorised loads; no staging).
 // ------------------------------------------------------------------------------------------
 template <int IN>
