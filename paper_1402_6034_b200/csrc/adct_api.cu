@@ -67,19 +67,24 @@ adct_status make_u8_map(CUtensorMap* map, const uint8_t* src, int64_t n, int64_t
 
 // int16 coefficient plane (adct_inverse's TMA path): same box, 2-byte elements (copied as UINT16 —
 // TMA moves bytes; the kernel reinterprets them)
-adct_status make_i16_map(CUtensorMap* map, const void* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
-                         int64_t img_stride) {
+// image-shaped plane of 2- or 4-byte elements, one 16 x 256-element box per warp tile
+adct_status make_plane_map(CUtensorMap* map, CUtensorMapDataType dt, const void* src, int64_t n, int64_t h,
+                           int64_t w, int64_t pitch, int64_t img_stride) {
   EncodeTiledFn enc = get_encode();
   if (!enc) return cuda_fail(cudaErrorNotSupported);
   cuuint64_t dims[3] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)n};
   cuuint64_t strides[2] = {(cuuint64_t)pitch, (cuuint64_t)img_stride};
   cuuint32_t box[3] = {TILE_W, TILE_H, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, 3, const_cast<void*>(src), dims, strides, box, estr,
+  CUresult r = enc(map, dt, 3, const_cast<void*>(src), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return cuda_fail(cudaErrorInvalidValue);
   return ADCT_OK;
+}
+adct_status make_i16_map(CUtensorMap* map, const void* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                         int64_t img_stride) {
+  return make_plane_map(map, CU_TENSOR_MAP_DATA_TYPE_UINT16, src, n, h, w, pitch, img_stride);
 }
 
 bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
@@ -199,12 +204,11 @@ adct_status launch_tma_kernel(K kern, const CUtensorMap& map, const P& params_in
 
 
 
-// Forward to an int16 plane with TMA bulk stores (k_forward_i16_tma): two tensor maps.
-adct_status launch_forward_tma(const CUtensorMap& map, const CUtensorMap& omap, const ForwardParams& params_in,
-                               cudaStream_t stream) {
-  ForwardParams params = params_in;
-  auto kern = k_forward_i16_tma<0>;
-  const int smem = fwdt_smem_bytes();
+// Kernels with an input and an output tensor map (TMA loads + TMA bulk stores).
+template <class K, class P>
+adct_status launch_tma2(K kern, const CUtensorMap& map, const CUtensorMap& omap, const P& params_in, int smem,
+                        cudaStream_t stream) {
+  P params = params_in;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return cuda_fail(e);
   int dev = 0, sms = 0, occ = 0;
@@ -225,6 +229,10 @@ adct_status launch_forward_tma(const CUtensorMap& map, const CUtensorMap& omap, 
   ++g_launches;
   e = cudaGetLastError();
   return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
+}
+adct_status launch_forward_tma(const CUtensorMap& map, const CUtensorMap& omap, const ForwardParams& p,
+                               cudaStream_t stream) {
+  return launch_tma2(k_forward_i16_tma<0>, map, omap, p, fwdt_smem_bytes(), stream);
 }
 
 // Compress launch: ring depth from the kernel's per-r configuration.
@@ -339,6 +347,22 @@ adct_status adct_inverse(const void* coef, adct_coef_t coef_t, int64_t n, int64_
   if (coef_t == ADCT_COEF_I16) {  // staged by TMA through the warp rings (HBM-bound path)
     CUtensorMap map;
     if ((st = make_i16_map(&map, coef, n, h, w, coef_pitch, coef_img_stride))) return st;
+#ifndef ADCT_INV_TMA_STORE
+#define ADCT_INV_TMA_STORE 1
+#endif
+    // reconstruction tiles leave through shared memory + TMA bulk stores.  Measured on B200: a bulk
+    // tensor store writes a row's last partial 16-byte chunk whole, so the u8 plane takes this path
+    // only when w is a multiple of 16 (tests/test_gpu_parity.py::test_no_writes_outside_outputs)
+    if (ADCT_INV_TMA_STORE && (dst_t == ADCT_RECON_F32 || (w & 15) == 0)) {
+      CUtensorMap omap;
+      if (dst_t == ADCT_RECON_F32) {
+        if ((st = make_plane_map(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, dst, n, h, w, dst_pitch, dst_img_stride)))
+          return st;
+        return launch_tma2(k_inverse_i16_tma<REC_F32>, map, omap, p, invt_smem_bytes(REC_F32), s0);
+      }
+      if ((st = make_u8_map(&omap, (const uint8_t*)dst, n, h, w, dst_pitch, dst_img_stride))) return st;
+      return launch_tma2(k_inverse_i16_tma<REC_U8>, map, omap, p, invt_smem_bytes(REC_U8), s0);
+    }
     return dst_t == ADCT_RECON_F32
                ? launch_tma_kernel(k_inverse_i16<REC_F32>, map, p, p.tiles, s0, 2, 2 * TILE_BYTES)
                : launch_tma_kernel(k_inverse_i16<REC_U8>, map, p, p.tiles, s0, 2, 2 * TILE_BYTES);

@@ -749,6 +749,92 @@ __global__ void __launch_bounds__(WARPS * 32, 3)
 }
 
 // ------------------------------------------------------------------------------------------
+// Inverse from an int16 plane with TMA bulk-tensor stores of the reconstruction: the warp's
+// 16 x 256 output tile (f32: 16 KiB, u8: 4 KiB) is staged in shared memory row by row and stored
+// by one elected lane; the staging buffer is rewritten only after the previous store has read it.
+// ------------------------------------------------------------------------------------------
+#ifndef ADCT_INVT_MINB
+#define ADCT_INVT_MINB 1
+#endif
+constexpr int invt_stage_bytes(int RECON) { return RECON == REC_F32 ? 4 * TILE_BYTES : TILE_BYTES; }
+constexpr int invt_smem_bytes(int RECON) {
+  return WARPS * 2 * (2 * TILE_BYTES) + FWDT_BAR_BYTES + WARPS * invt_stage_bytes(RECON);
+}
+template <int RECON>
+__device__ __forceinline__ void stage_recon_row(uint8_t* buf, int row_a, int lane, const float2 (&x)[8]) {
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    const int row = row_a + 8 * b;
+    if constexpr (RECON == REC_F32) {
+      float v[8];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) v[n] = (b ? x[n].y : x[n].x) * (1.0f / 576.0f);
+      float4* q = reinterpret_cast<float4*>(buf + row * (4 * TILE_W) + lane * 32);
+      q[0] = make_float4(v[0], v[1], v[2], v[3]);
+      q[1] = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+      uint32_t u[8];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        const float y = ((b ? x[n].y : x[n].x) + 288.5f) * (1.0f / 576.0f);
+        u[n] = __float_as_uint(__fadd_rz(fminf(fmaxf(y, 0.f), 255.f), 8388608.0f));
+      }
+      uint2 o;
+      o.x = __byte_perm(__byte_perm(u[0], u[1], 0x0040), __byte_perm(u[2], u[3], 0x0040), 0x5410);
+      o.y = __byte_perm(__byte_perm(u[4], u[5], 0x0040), __byte_perm(u[6], u[7], 0x0040), 0x5410);
+      *reinterpret_cast<uint2*>(buf + row * TILE_W + lane * 8) = o;
+    }
+  }
+}
+template <int RECON>
+__global__ void __launch_bounds__(WARPS * 32, ADCT_INVT_MINB)
+    k_inverse_i16_tma(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
+                      const __grid_constant__ InverseParams p) {
+  constexpr int TB = 2 * TILE_BYTES;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  uint8_t* ring = smem + warp * (2 * TB);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * 2 * TB) + warp * 2;
+  uint8_t* buf = smem + WARPS * 2 * TB + FWDT_BAR_BYTES + warp * invt_stage_bytes(RECON);
+  const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
+  tma_ring_loop_u<2, TB>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
+                         [&](const uint8_t* tile, int img, int ty, int tx) {
+    float2 V[64];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint4 a = *reinterpret_cast<const uint4*>(tile + (k * TILE_W + lane * 8) * 2);
+      const uint4 b = *reinterpret_cast<const uint4*>(tile + ((k + 8) * TILE_W + lane * 8) * 2);
+      const uint32_t wa[4] = {a.x ^ 0x80008000u, a.y ^ 0x80008000u, a.z ^ 0x80008000u, a.w ^ 0x80008000u};
+      const uint32_t wb[4] = {b.x ^ 0x80008000u, b.y ^ 0x80008000u, b.z ^ 0x80008000u, b.w ^ 0x80008000u};
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int kl = k * 8 + 2 * m + h;
+          const uint32_t P = __byte_perm(wa[m], wb[m], h ? 0x7632 : 0x5410);  // (A + 2^15) | (B + 2^15) << 16
+          V[kl] = f2fma(biased_pair(P), f2(p.tab.w[kl].x), f2(p.tab.c[kl].x));  // w Y (0 if masked)
+        }
+      }
+    }
+    if (lane == 0) bulk_wait_read<0>();  // the previous tile's store has finished reading `buf`
+    __syncwarp();
+    inverse2d<RT>(V, [&](auto Ic, auto row) {
+      constexpr int I = decltype(Ic)::value;
+      float2 xr[8];
+      static_for<8>([&](auto Nc) {
+        constexpr int N = decltype(Nc)::value;
+        xr[N] = val(cuda::std::get<N>(row));
+      });
+      stage_recon_row<RECON>(buf, I, lane, xr);
+    });
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) bulk_store_3d(&omap, smem_u32(buf), tx * TILE_W, ty * TILE_H, img);
+  });
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// ------------------------------------------------------------------------------------------
 // Dense comparator path: any 8x8 transform T as dense fp32 products — the
 // exact DCT (the paper's reference curve), the SDCT sign(C)/(2 sqrt2) (P:78,
 // P:288-289), the coarse C0/2 or a caller matrix.  Per block: Z = T X T^T, keep the

@@ -545,8 +545,9 @@ def _outside(big, n, h, w):
     return big[m]
 
 
-@pytest.mark.parametrize("n,h,w", [(3, 40, 264), (1, 8, 8), (2, 24, 520), (2, 16, 256)])
+@pytest.mark.parametrize("n,h,w", [(3, 40, 264), (1, 8, 8), (2, 24, 520), (2, 16, 256), (3, 40, 272)])
 def test_no_writes_outside_outputs(n, h, w):
+    # (3, 40, 272): ragged tile rows and columns on the TMA bulk-store paths (w % 16 == 0)
     x = dev(rng.integers(0, 256, (n, h, w), dtype=np.uint8))
     canary_f, canary_u, canary_i = -12345.5, 77, -4321
     # per-image arrays: a canary tail after the n entries
