@@ -418,8 +418,24 @@ adct_status adct_compress_psnr(const uint8_t* src, int64_t n, int64_t h, int64_t
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(double) * (size_t)n, s);
   if (e != cudaSuccess) return cuda_fail(e);
+#ifndef ADCT_RECON_TMA_STORE
+#define ADCT_RECON_TMA_STORE 1
+#endif
+  // reconstruction through shared-memory staging + TMA bulk stores (u8: only for w % 16 == 0, a
+  // bulk store writes a row's last partial 16-byte chunk whole)
+  const bool bulk = ADCT_RECON_TMA_STORE && (recon_t == ADCT_RECON_F32 || (recon_t == ADCT_RECON_U8 && (w & 15) == 0));
+  CUtensorMap omap;
+  if (bulk) {
+    st = recon_t == ADCT_RECON_F32
+             ? make_plane_map(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, recon, n, h, w, recon_pitch, recon_img_stride)
+             : make_u8_map(&omap, (const uint8_t*)recon, n, h, w, recon_pitch, recon_img_stride);
+    if (st) return st;
+  }
   if (q > 0.f) {
     fill_quant_tables(p.tab, r, q);
+    if (bulk && recon_t == ADCT_RECON_F32)
+      return launch_tma2(k_compress_recon<MODE_QUANT, REC_F32>, map, omap, p, crec_smem_bytes(REC_F32), s);
+    if (bulk) return launch_tma2(k_compress_recon<MODE_QUANT, REC_U8>, map, omap, p, crec_smem_bytes(REC_U8), s);
     if (recon_t == ADCT_RECON_NONE && r == 64)  // C4's case: compile-time mask, per-class constants
       return launch_compress(k_compress<64, MODE_QUANT, REC_NONE>, 64, map, p, s);
     if (recon_t == ADCT_RECON_NONE) return launch_compress(k_compress<RT, MODE_QUANT, REC_NONE>, RT, map, p, s);
@@ -430,6 +446,9 @@ adct_status adct_compress_psnr(const uint8_t* src, int64_t n, int64_t h, int64_t
   if (recon_t == ADCT_RECON_NONE) {
     return launch_compress(zonal_kernel(r), r, map, p, s);
   }
+  if (bulk && recon_t == ADCT_RECON_F32)
+    return launch_tma2(k_compress_recon<MODE_ZONAL, REC_F32>, map, omap, p, crec_smem_bytes(REC_F32), s);
+  if (bulk) return launch_tma2(k_compress_recon<MODE_ZONAL, REC_U8>, map, omap, p, crec_smem_bytes(REC_U8), s);
   if (recon_t == ADCT_RECON_F32) return launch_compress(k_compress<RT, MODE_ZONAL, REC_F32>, RT, map, p, s);
   return launch_compress(k_compress<RT, MODE_ZONAL, REC_U8>, RT, map, p, s);
 }

@@ -117,6 +117,37 @@ __device__ __forceinline__ void store_recon_row(uint8_t* base, int64_t pitch, in
   }
 }
 
+// The same two output rows into a warp-private shared-memory staging tile laid out as the 16 x 256
+// box of a TMA bulk-tensor store (f32: 1 KiB per row, u8: 256 B per row).
+template <int RECON, bool S576>
+__device__ __forceinline__ void stage_recon_row(uint8_t* buf, int row_a, int lane, const float2 (&x)[8]) {
+#pragma unroll
+  for (int b = 0; b < 2; ++b) {
+    const int row = row_a + 8 * b;
+    if constexpr (RECON == REC_F32) {
+      float v[8];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) v[n] = S576 ? (b ? x[n].y : x[n].x) * (1.0f / 576.0f) : (b ? x[n].y : x[n].x);
+      float4* q = reinterpret_cast<float4*>(buf + row * (4 * TILE_W) + lane * 32);
+      q[0] = make_float4(v[0], v[1], v[2], v[3]);
+      q[1] = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+      uint32_t u[8];
+#pragma unroll
+      for (int n = 0; n < 8; ++n) {
+        const float xv = b ? x[n].y : x[n].x;
+        const float y = S576 ? (xv + 288.5f) * (1.0f / 576.0f) : xv + 0.5f;
+        u[n] = __float_as_uint(__fadd_rz(fminf(fmaxf(y, 0.f), 255.f), 8388608.0f));
+      }
+      uint2 o;
+      o.x = __byte_perm(__byte_perm(u[0], u[1], 0x0040), __byte_perm(u[2], u[3], 0x0040), 0x5410);
+      o.y = __byte_perm(__byte_perm(u[4], u[5], 0x0040), __byte_perm(u[6], u[7], 0x0040), 0x5410);
+      *reinterpret_cast<uint2*>(buf + row * TILE_W + lane * 8) = o;
+    }
+  }
+}
+constexpr int recon_stage_bytes(int RECON) { return RECON == REC_F32 ? 4 * TILE_BYTES : TILE_BYTES; }
+
 // ------------------------------------------------------------------------------------------
 // Fused compress path, split in two halves so that a warp can overlap the ALU-heavy forward of
 // tile j+1 (SWAR IADD3/PRMT) with the FMA-heavy inverse + error of tile j (FADD2/FFMA2) in one
@@ -170,9 +201,10 @@ template <int N> __device__ __forceinline__ float2 err_fh(uint32_t ha, uint32_t 
   return err_fh<N, true>(ha, hb, r.v);
 }
 
-template <int R, int MODE, int RECON, int F16 = 0, bool GROUPED = false>
+template <int R, int MODE, int RECON, int F16 = 0, bool GROUPED = false, bool STAGE = false>
 __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const uint8_t* tile, int lane,
-                                               const CompressParams& p, int img, int ty, int tx) {
+                                               const CompressParams& p, int img, int ty, int tx,
+                                               uint8_t* sbuf = nullptr) {
   constexpr int RF = R;
   static_assert(F16 == 0 || (MODE == MODE_ZONAL && RECON == REC_NONE && RF < RT), "f16 error route: zonal SSE only");
   float2 V[64];
@@ -233,7 +265,8 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
         if constexpr (RECON != REC_NONE) xr[N] = val(get<N>(row));
       }
     });
-    if constexpr (RECON != REC_NONE)
+    if constexpr (RECON != REC_NONE && STAGE) stage_recon_row<RECON, (MODE == MODE_ZONAL)>(sbuf, I, lane, xr);
+    else if constexpr (RECON != REC_NONE)
       store_recon_row<RECON, (MODE == MODE_ZONAL)>(rbase, p.recon_pitch, p.h, p.w, ty * TILE_H + I, col, xr);
   };
   if constexpr (GROUPED) inverse2d_grouped<RF>(V, err_row);
@@ -761,32 +794,6 @@ constexpr int invt_smem_bytes(int RECON) {
   return WARPS * 2 * (2 * TILE_BYTES) + FWDT_BAR_BYTES + WARPS * invt_stage_bytes(RECON);
 }
 template <int RECON>
-__device__ __forceinline__ void stage_recon_row(uint8_t* buf, int row_a, int lane, const float2 (&x)[8]) {
-#pragma unroll
-  for (int b = 0; b < 2; ++b) {
-    const int row = row_a + 8 * b;
-    if constexpr (RECON == REC_F32) {
-      float v[8];
-#pragma unroll
-      for (int n = 0; n < 8; ++n) v[n] = (b ? x[n].y : x[n].x) * (1.0f / 576.0f);
-      float4* q = reinterpret_cast<float4*>(buf + row * (4 * TILE_W) + lane * 32);
-      q[0] = make_float4(v[0], v[1], v[2], v[3]);
-      q[1] = make_float4(v[4], v[5], v[6], v[7]);
-    } else {
-      uint32_t u[8];
-#pragma unroll
-      for (int n = 0; n < 8; ++n) {
-        const float y = ((b ? x[n].y : x[n].x) + 288.5f) * (1.0f / 576.0f);
-        u[n] = __float_as_uint(__fadd_rz(fminf(fmaxf(y, 0.f), 255.f), 8388608.0f));
-      }
-      uint2 o;
-      o.x = __byte_perm(__byte_perm(u[0], u[1], 0x0040), __byte_perm(u[2], u[3], 0x0040), 0x5410);
-      o.y = __byte_perm(__byte_perm(u[4], u[5], 0x0040), __byte_perm(u[6], u[7], 0x0040), 0x5410);
-      *reinterpret_cast<uint2*>(buf + row * TILE_W + lane * 8) = o;
-    }
-  }
-}
-template <int RECON>
 __global__ void __launch_bounds__(WARPS * 32, ADCT_INVT_MINB)
     k_inverse_i16_tma(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
                       const __grid_constant__ InverseParams p) {
@@ -825,12 +832,56 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INVT_MINB)
         constexpr int N = decltype(Nc)::value;
         xr[N] = val(cuda::std::get<N>(row));
       });
-      stage_recon_row<RECON>(buf, I, lane, xr);
+      stage_recon_row<RECON, true>(buf, I, lane, xr);
     });
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) bulk_store_3d(&omap, smem_u32(buf), tx * TILE_W, ty * TILE_H, img);
   });
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// ------------------------------------------------------------------------------------------
+// Fused compress with a reconstruction output (runtime mask / quantiser, f32 or u8): the warp's
+// reconstruction tile is staged in shared memory and leaves through one TMA bulk-tensor store.
+// ------------------------------------------------------------------------------------------
+constexpr int crec_smem_bytes(int RECON) {
+  return WARPS * 2 * TILE_BYTES + FWDT_BAR_BYTES + WARPS * recon_stage_bytes(RECON);
+}
+template <int MODE, int RECON>
+__global__ void __launch_bounds__(WARPS * 32, ADCT_MINB_RT)
+    k_compress_recon(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
+                     const __grid_constant__ CompressParams p) {
+  constexpr int ST = 2;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const double kSseScale = (MODE == MODE_ZONAL) ? 1.0 / 331776.0 : 1.0;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  uint8_t* ring = smem + warp * (ST * TILE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * ST * TILE_BYTES) + warp * ST;
+  uint8_t* buf = smem + WARPS * ST * TILE_BYTES + FWDT_BAR_BYTES + warp * recon_stage_bytes(RECON);
+  const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
+  int cur = -1;
+  double acc = 0.0;
+  tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
+                      [&](const uint8_t* tile, int img, int ty, int tx) {
+    if (img != cur) {  // warp-uniform: flush the finished image's partial SSE
+      const double v = warp_sum(acc);
+      if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v * kSseScale);
+      cur = img;
+      acc = 0.0;
+    }
+    uint32_t Y[8][8];
+    compress_fwd<RT, MODE>(tile, lane, Y);
+    if (lane == 0) bulk_wait_read<0>();  // the previous tile's store has finished reading `buf`
+    __syncwarp();
+    const float2 e2 = compress_inv<RT, MODE, RECON, 0, false, true>(Y, tile, lane, p, img, ty, tx, buf);
+    acc += (double)e2.x + (double)e2.y;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) bulk_store_3d(&omap, smem_u32(buf), tx * TILE_W, ty * TILE_H, img);
+  });
+  const double v = warp_sum(acc);
+  if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v * kSseScale);
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
