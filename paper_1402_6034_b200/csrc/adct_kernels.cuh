@@ -81,15 +81,59 @@ struct InverseParams {
 // ------------------------------------------------------------------------------------------
 // Reconstruction store for row I (8 pixels of block A and of block B) — masked to the image.
 // ------------------------------------------------------------------------------------------
+// u8 reconstruction of one output row of both blocks, x[n] = (A, B) pair of pixel n.
+// S576: u8 = clamp(round_half_away(R / 576)) = clamp(floor((R + 288.5) / 576)) for integer R
+// (never within 8.7e-4 of an integer, so the fp32 product is floored exactly); else clamp(floor(x^ + 0.5)).
+// One FADD2 + one round-toward-zero FFMA2 with the magic 2^23 + 512 per pixel pair puts
+// floor(y) + 512 in the low 16 bits; two halves pack into one word, clamp to [512, 767] with
+// VIMNMX.U16x2, and the low bytes are floor(y) clamped to [0, 255].
+template <bool S576>
+__device__ __forceinline__ void u8_rows(const float2 (&x)[8], uint2& ra, uint2& rb) {
+  uint32_t ta[8], tb[8];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) {
+    float2 t;
+    if constexpr (S576) {
+      const float2 sft = f2add(x[n], f2(288.5f));  // exact: R is an integer below 2^19
+      unsigned long long d;
+      asm("fma.rz.f32x2 %0, %1, %2, %3;" : "=l"(d)
+          : "l"(*reinterpret_cast<const unsigned long long*>(&sft)), "l"(0x3AE38E393AE38E39ull),
+            "l"(0x4B0002004B000200ull));
+      t = *reinterpret_cast<float2*>(&d);
+    } else {
+      const float2 y = f2add(x[n], f2(0.5f));
+      unsigned long long d;
+      asm("add.rz.f32x2 %0, %1, %2;" : "=l"(d)
+          : "l"(*reinterpret_cast<const unsigned long long*>(&y)), "l"(0x4B0002004B000200ull));
+      t = *reinterpret_cast<float2*>(&d);
+    }
+    ta[n] = __float_as_uint(t.x);
+    tb[n] = __float_as_uint(t.y);
+  }
+  uint32_t pa[4], pb[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    pa[q] = __byte_perm(ta[2 * q], ta[2 * q + 1], 0x5410);
+    pb[q] = __byte_perm(tb[2 * q], tb[2 * q + 1], 0x5410);
+    asm("max.u16x2 %0, %0, %1;" : "+r"(pa[q]) : "r"(0x02000200u));
+    asm("min.u16x2 %0, %0, %1;" : "+r"(pa[q]) : "r"(0x02FF02FFu));
+    asm("max.u16x2 %0, %0, %1;" : "+r"(pb[q]) : "r"(0x02000200u));
+    asm("min.u16x2 %0, %0, %1;" : "+r"(pb[q]) : "r"(0x02FF02FFu));
+  }
+  ra = make_uint2(__byte_perm(pa[0], pa[1], 0x6420), __byte_perm(pa[2], pa[3], 0x6420));
+  rb = make_uint2(__byte_perm(pb[0], pb[1], 0x6420), __byte_perm(pb[2], pb[3], 0x6420));
+}
+
 template <int RECON, bool S576>
 __device__ __forceinline__ void store_recon_row(uint8_t* base, int64_t pitch, int h, int w, int row_a,
                                                 int col, const float2 (&x)[8]) {
   // S576: x[n] = (R_A[n], R_B[n]) with R = 576 x^ exactly (integers in fp32); else x[n] = x^ itself
   if (col >= w) return;
+  if (RECON == REC_U8 && row_a >= h) return;
   const int rows[2] = {row_a, row_a + 8};
 #pragma unroll
   for (int b = 0; b < 2; ++b) {
-    if (rows[b] >= h) continue;
+    if (RECON == REC_U8 || rows[b] >= h) continue;
     uint8_t* p = base + (int64_t)rows[b] * pitch;
     if constexpr (RECON == REC_F32) {
       float v[8];
@@ -98,22 +142,13 @@ __device__ __forceinline__ void store_recon_row(uint8_t* base, int64_t pitch, in
       float4* q = reinterpret_cast<float4*>(p + (int64_t)col * 4);
       q[0] = make_float4(v[0], v[1], v[2], v[3]);
       q[1] = make_float4(v[4], v[5], v[6], v[7]);
-    } else {
-      uint32_t u[8];
-#pragma unroll
-      for (int n = 0; n < 8; ++n) {
-        // round_half_away(R / 576) then clamp: floor((R + 288.5) / 576) is exact for integer R.
-        // floor of the clamped value through the 2^23 magic with a round-toward-zero add (FMA pipe):
-        // the low byte of the sum's bits is the integer part — no float->int conversion unit.
-        const float xv = b ? x[n].y : x[n].x;
-        const float y = S576 ? (xv + 288.5f) * (1.0f / 576.0f) : xv + 0.5f;
-        u[n] = __float_as_uint(__fadd_rz(fminf(fmaxf(y, 0.f), 255.f), 8388608.0f));
-      }
-      uint2 o;  // pack the low bytes
-      o.x = __byte_perm(__byte_perm(u[0], u[1], 0x0040), __byte_perm(u[2], u[3], 0x0040), 0x5410);
-      o.y = __byte_perm(__byte_perm(u[4], u[5], 0x0040), __byte_perm(u[6], u[7], 0x0040), 0x5410);
-      *reinterpret_cast<uint2*>(p + col) = o;
     }
+  }
+  if constexpr (RECON == REC_U8) {
+    uint2 ra, rb;
+    u8_rows<S576>(x, ra, rb);
+    *reinterpret_cast<uint2*>(base + (int64_t)row_a * pitch + col) = ra;
+    if (row_a + 8 < h) *reinterpret_cast<uint2*>(base + (int64_t)(row_a + 8) * pitch + col) = rb;
   }
 }
 
@@ -131,19 +166,13 @@ __device__ __forceinline__ void stage_recon_row(uint8_t* buf, int row_a, int lan
       float4* q = reinterpret_cast<float4*>(buf + row * (4 * TILE_W) + lane * 32);
       q[0] = make_float4(v[0], v[1], v[2], v[3]);
       q[1] = make_float4(v[4], v[5], v[6], v[7]);
-    } else {
-      uint32_t u[8];
-#pragma unroll
-      for (int n = 0; n < 8; ++n) {
-        const float xv = b ? x[n].y : x[n].x;
-        const float y = S576 ? (xv + 288.5f) * (1.0f / 576.0f) : xv + 0.5f;
-        u[n] = __float_as_uint(__fadd_rz(fminf(fmaxf(y, 0.f), 255.f), 8388608.0f));
-      }
-      uint2 o;
-      o.x = __byte_perm(__byte_perm(u[0], u[1], 0x0040), __byte_perm(u[2], u[3], 0x0040), 0x5410);
-      o.y = __byte_perm(__byte_perm(u[4], u[5], 0x0040), __byte_perm(u[6], u[7], 0x0040), 0x5410);
-      *reinterpret_cast<uint2*>(buf + row * TILE_W + lane * 8) = o;
     }
+  }
+  if constexpr (RECON == REC_U8) {
+    uint2 ra, rb;
+    u8_rows<S576>(x, ra, rb);
+    *reinterpret_cast<uint2*>(buf + row_a * TILE_W + lane * 8) = ra;
+    *reinterpret_cast<uint2*>(buf + (row_a + 8) * TILE_W + lane * 8) = rb;
   }
 }
 constexpr int recon_stage_bytes(int RECON) { return RECON == REC_F32 ? 4 * TILE_BYTES : TILE_BYTES; }
