@@ -230,9 +230,13 @@ adct_status launch_tma2(K kern, const CUtensorMap& map, const CUtensorMap& omap,
   e = cudaGetLastError();
   return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
 }
-adct_status launch_forward_tma(const CUtensorMap& map, const CUtensorMap& omap, const ForwardParams& p,
-                               cudaStream_t stream) {
-  return launch_tma2(k_forward_i16_tma<0>, map, omap, p, fwdt_smem_bytes(), stream);
+adct_status launch_forward_tma(adct_coef_t coef_t, const CUtensorMap& map, const CUtensorMap& omap,
+                               const ForwardParams& p, cudaStream_t stream) {
+  switch (coef_t) {
+    case ADCT_COEF_I16: return launch_tma2(k_forward_tma<OUT_I16>, map, omap, p, fwdt_smem_bytes(OUT_I16), stream);
+    case ADCT_COEF_I32: return launch_tma2(k_forward_tma<OUT_I32>, map, omap, p, fwdt_smem_bytes(OUT_I32), stream);
+    default: return launch_tma2(k_forward_tma<OUT_F32>, map, omap, p, fwdt_smem_bytes(OUT_F32), stream);
+  }
 }
 
 // Compress launch: ring depth from the kernel's per-r configuration.
@@ -295,18 +299,20 @@ adct_status adct_forward(const uint8_t* src, int64_t n, int64_t h, int64_t w, in
     for (int l = 0; l < 8; ++l)
       p.sc[k * 8 + l] = (zz_host(k, l) < r) ? (float)(1.0 / sqrt(dd_host(k, l))) : 0.f;
   cudaStream_t s = (cudaStream_t)stream;
-  switch (coef_t) {
-    case ADCT_COEF_I16: {
 #ifndef ADCT_FWD_TMA_STORE
 #define ADCT_FWD_TMA_STORE 1
 #endif
-      if (ADCT_FWD_TMA_STORE) {
-        CUtensorMap omap;
-        if ((st = make_i16_map(&omap, coef, n, h, w, coef_pitch, coef_img_stride))) return st;
-        return launch_forward_tma(map, omap, p, s);
-      }
-      return launch_tma_kernel(k_forward<OUT_I16>, map, p, p.tiles, s, FWD_ST);
-    }
+  if (ADCT_FWD_TMA_STORE) {  // coefficient tiles leave through shared memory + TMA bulk stores
+    CUtensorMap omap;
+    st = make_plane_map(&omap,
+                        coef_t == ADCT_COEF_I16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                        : coef_t == ADCT_COEF_I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                        coef, n, h, w, coef_pitch, coef_img_stride);
+    if (st) return st;
+    return launch_forward_tma(coef_t, map, omap, p, s);
+  }
+  switch (coef_t) {
+    case ADCT_COEF_I16: return launch_tma_kernel(k_forward<OUT_I16>, map, p, p.tiles, s, FWD_ST);
     case ADCT_COEF_I32: return launch_tma_kernel(k_forward<OUT_I32>, map, p, p.tiles, s, FWD_ST);
     default: return launch_tma_kernel(k_forward<OUT_F32>, map, p, p.tiles, s, FWD_ST);
   }

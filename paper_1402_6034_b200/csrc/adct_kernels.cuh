@@ -645,9 +645,14 @@ __global__ void __launch_bounds__(WARPS * 32, FWD_MINB)
 #ifndef ADCT_FWDT_MINB
 #define ADCT_FWDT_MINB 2
 #endif
-constexpr int FWDT_ST = ADCT_FWDT_ST, FWDT_NSTG = ADCT_FWDT_NSTG;
+constexpr int FWDT_ST = ADCT_FWDT_ST;
 constexpr int FWDT_BAR_BYTES = 128;  // mbarriers, padded so the staging buffers stay 128-B aligned
-constexpr int fwdt_smem_bytes() { return WARPS * FWDT_ST * TILE_BYTES + FWDT_BAR_BYTES + WARPS * FWDT_NSTG * 2 * TILE_BYTES; }
+// staging per warp tile: int16 8 KiB (double-buffered), int32 / f32 16 KiB (single: 2 CTAs per SM)
+constexpr int fwdt_nstg(int OUT) { return OUT == OUT_I16 ? ADCT_FWDT_NSTG : 1; }
+constexpr int fwdt_tile_out_bytes(int OUT) { return OUT == OUT_I16 ? 2 * TILE_BYTES : 4 * TILE_BYTES; }
+constexpr int fwdt_smem_bytes(int OUT) {
+  return WARPS * FWDT_ST * TILE_BYTES + FWDT_BAR_BYTES + WARPS * fwdt_nstg(OUT) * fwdt_tile_out_bytes(OUT);
+}
 __device__ __forceinline__ void bulk_store_3d(const CUtensorMap* map, uint32_t src, int x, int y, int z) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)), "r"(src), "r"(x), "r"(y), "r"(z)
@@ -657,47 +662,72 @@ __device__ __forceinline__ void bulk_store_3d(const CUtensorMap* map, uint32_t s
 template <int N> __device__ __forceinline__ void bulk_wait_read() {
   asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
-template <int UNUSED = 0>
+template <int OUT>
 __global__ void __launch_bounds__(WARPS * 32, ADCT_FWDT_MINB)
-    k_forward_i16_tma(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
-                      const __grid_constant__ ForwardParams p) {
+    k_forward_tma(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
+                  const __grid_constant__ ForwardParams p) {
+  constexpr int NSTG = fwdt_nstg(OUT), OB = fwdt_tile_out_bytes(OUT);
+  constexpr uint32_t K = (OUT == OUT_F32) ? BIAS2 : 0x8000u;
   extern __shared__ __align__(128) uint8_t smem[];
   static_assert(WARPS * FWDT_ST * 8 <= FWDT_BAR_BYTES, "mbarrier area");
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   uint8_t* ring = smem + warp * (FWDT_ST * TILE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * FWDT_ST * TILE_BYTES) + warp * FWDT_ST;
-  uint8_t* stg = smem + WARPS * FWDT_ST * TILE_BYTES + FWDT_BAR_BYTES + warp * (FWDT_NSTG * 2 * TILE_BYTES);
+  uint8_t* stg = smem + WARPS * FWDT_ST * TILE_BYTES + FWDT_BAR_BYTES + warp * (NSTG * OB);
   const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
   int sidx = 0;
   tma_ring_loop_u<FWDT_ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
                            [&](const uint8_t* tile, int img, int ty, int tx) {
-    uint8_t* buf = stg + sidx * (2 * TILE_BYTES);
+    uint8_t* buf = stg + sidx * OB;
     uint32_t P[8][8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
       pack_rows(lds64(tile + i * TILE_W + lane * 8), lds64(tile + (i + 8) * TILE_W + lane * 8), P[i]);
     uint32_t Y[8][8];
-    fwd2d<0x8000u, 64>(P, Y);
-    if (lane == 0) bulk_wait_read<FWDT_NSTG - 1>();  // the store that last read `buf` is done reading
+    fwd2d<K, 64>(P, Y);
+    if (lane == 0) bulk_wait_read<NSTG - 1>();  // the store that last read `buf` is done reading
     __syncwarp();
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
-        uint32_t o[4];
+        uint8_t* row = buf + (b * 8 + k) * (OB / TILE_H);
+        if constexpr (OUT == OUT_I16) {
+          uint32_t o[4];
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
-          o[m] = b ? __byte_perm(Y[k][2 * m], Y[k][2 * m + 1], 0x7632)
-                   : (__byte_perm(Y[k][2 * m], Y[k][2 * m + 1], 0x5410) ^ 0x80008000u);
-          if (p.masked) o[m] &= p.m16[k * 4 + m];
+          for (int m = 0; m < 4; ++m) {
+            o[m] = b ? __byte_perm(Y[k][2 * m], Y[k][2 * m + 1], 0x7632)
+                     : (__byte_perm(Y[k][2 * m], Y[k][2 * m + 1], 0x5410) ^ 0x80008000u);
+            if (p.masked) o[m] &= p.m16[k * 4 + m];
+          }
+          *reinterpret_cast<uint4*>(row + lane * 16) = make_uint4(o[0], o[1], o[2], o[3]);
+        } else if constexpr (OUT == OUT_I32) {
+          int v[8];
+#pragma unroll
+          for (int l = 0; l < 8; ++l) {
+            v[l] = b ? ((int32_t)Y[k][l] >> 16) : ((int)(Y[k][l] & 0xFFFFu) - 32768);
+            if (p.masked && !((p.keep_raster >> (k * 8 + l)) & 1ull)) v[l] = 0;
+          }
+          int4* q = reinterpret_cast<int4*>(row + lane * 32);
+          q[0] = make_int4(v[0], v[1], v[2], v[3]);
+          q[1] = make_int4(v[4], v[5], v[6], v[7]);
+        } else {
+          float v[8];
+#pragma unroll
+          for (int l = 0; l < 8; ++l) {
+            const float2 y = f2add(biased_pair(Y[k][l]), f2(-KF));
+            v[l] = (b ? y.y : y.x) * p.sc[k * 8 + l];
+          }
+          float4* q = reinterpret_cast<float4*>(row + lane * 32);
+          q[0] = make_float4(v[0], v[1], v[2], v[3]);
+          q[1] = make_float4(v[4], v[5], v[6], v[7]);
         }
-        *reinterpret_cast<uint4*>(buf + (b * 8 + k) * (2 * TILE_W) + lane * 16) = make_uint4(o[0], o[1], o[2], o[3]);
       }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic-proxy writes -> bulk copy
     __syncwarp();
     if (lane == 0) bulk_store_3d(&omap, smem_u32(buf), tx * TILE_W, ty * TILE_H, img);
-    if constexpr (FWDT_NSTG > 1) sidx = (sidx + 1 == FWDT_NSTG) ? 0 : sidx + 1;
+    if constexpr (NSTG > 1) sidx = (sidx + 1 == NSTG) ? 0 : sidx + 1;
   });
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }

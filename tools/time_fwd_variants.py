@@ -28,10 +28,16 @@ def best(fn):
         e1.record(); torch.cuda.synchronize(); b = min(b, e0.elapsed_time(e1) / 10)
     return b
 ms = best(lambda: A.forward(x, out=out))
+o32 = torch.empty((4096, 512, 512), dtype=torch.int32, device="cuda")
+of = torch.empty((4096, 512, 512), dtype=torch.float32, device="cuda")
+ms32 = best(lambda: A.forward(x[:4096], coef="i32", out=o32))
+msf = best(lambda: A.forward(x[:4096], coef="f32", out=of))
 ck = [int(out.view(torch.int32).sum(dtype=torch.int64).item()), int(out[:, ::7, ::5].to(torch.int64).pow(2).sum().item())]
 masked = A.forward(x[:64], r=10)
 ck.append(int(masked.to(torch.int64).abs().sum().item()))
-print(json.dumps({"lib": __LIBV__, "ms": ms, "ck": ck}))
+ck.append(int(o32[:, ::3, ::5].to(torch.int64).abs().sum().item()))
+ck.append(float(of[:, ::3, ::5].double().abs().sum().item()))
+print(json.dumps({"lib": __LIBV__, "ms": ms, "ms32": ms32, "msf": msf, "ck": ck}))
 '''
 
 
@@ -48,7 +54,10 @@ def main():
     px = 8192 * 512 * 512
     for d in res:
         gbs = 3 * px / (d["ms"] * 1e-3) / 1e9
-        print(f"{os.path.basename(d['lib']):22s} C3 forward: {d['ms']:.3f} ms  {gbs:.0f} GB/s  frac {gbs / peak:.3f}  "
+        g32 = 5 * px / 2 / (d["ms32"] * 1e-3) / 1e9
+        gf = 5 * px / 2 / (d["msf"] * 1e-3) / 1e9
+        print(f"{os.path.basename(d['lib']):22s} C3 forward i16: {d['ms']:.3f} ms  {gbs:.0f} GB/s  frac {gbs / peak:.3f} | "
+              f"i32 (4096 img): frac {g32 / peak:.3f} | f32: frac {gf / peak:.3f} | "
               f"output {'identical' if d['ck'] == res[0]['ck'] else 'DIFFERENT'}")
 
 
