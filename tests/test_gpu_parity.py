@@ -285,6 +285,42 @@ def test_compress_sse576_c5_images_bit_exact():
         assert np.all(np.abs(fused - exact / 576.0 ** 2) <= SSE_RTOL * exact / 576.0 ** 2)
 
 
+def test_cuda_graph_capture_and_replay():
+    """Every entry is stream-ordered with host-side argument encoding only, so a sequence of calls
+    can be captured into a CUDA graph and replayed (the tensor maps travel as kernel parameters)."""
+    imgs = S.corpus_c2(3, 128, 256)
+    x = dev(imgs)
+    sse = torch.empty((4, 3), dtype=torch.float64, device="cuda")
+    ps = torch.empty((4, 3), dtype=torch.float64, device="cuda")
+    rs = (1, 10, 36)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):  # warm-up outside the capture (first-call attribute setup)
+        for k, r in enumerate(rs):
+            A.compress_psnr(x, r, sse=sse[k])
+        A.compress_psnr(x, 64, q=16.0, sse=sse[3])
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for k, r in enumerate(rs):
+            A.compress_psnr(x, r, sse=sse[k])
+        A.compress_psnr(x, 64, q=16.0, sse=sse[3])
+        A.psnr(sse.view(-1), 128 * 256, out=ps.view(-1))
+    sse.fill_(-1.0)
+    g.replay()
+    got = host(sse)
+    for k, r in enumerate(rs):
+        check_sse(got[k], O.compress_zonal_sse(imgs, r), 128 * 256)
+    check_sse(got[3], O.compress_quant_sse(imgs, 16.0), 128 * 256)
+    assert np.allclose(host(ps), O.psnr(got, 128 * 256), rtol=1e-12)
+    x.copy_(dev(imgs[::-1].copy()))  # replay on new data in the same buffers
+    g.replay()
+    got2 = host(sse)
+    for k, r in enumerate(rs):
+        check_sse(got2[k], O.compress_zonal_sse(imgs[::-1].copy(), r), 128 * 256)
+
+
 # ------------------------------------------------------------------ fused compress (quantiser)
 
 @pytest.mark.parametrize("q", [16.0, 5.0, 3.0])
