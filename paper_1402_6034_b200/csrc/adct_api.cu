@@ -3,6 +3,9 @@
 #include "adct.h"
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 #include "adct_kernels.cuh"
 
 namespace adct {
@@ -174,20 +177,49 @@ void fill_quant_tables(Tables& t, int r, float q) {
   t.qscale = (float)(((double)q / 8.0) * ((double)q / 8.0));
 }
 
+// Per (kernel, dynamic shared memory, device): the max-dynamic-smem attribute is set once and the
+// resident-CTA count and SM count are remembered, so a call costs no occupancy query (host time
+// per small call, profiles/r01_latency_c1.txt).  Thread-safe; entries are never removed.
+struct LaunchShape {
+  int sms, occ;
+};
+adct_status launch_shape(const void* kern, int smem, LaunchShape* out) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, int>, LaunchShape> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e);
+  const auto key = std::make_tuple(kern, smem, dev);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *out = it->second;
+      return ADCT_OK;
+    }
+  }
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return cuda_fail(e);
+  LaunchShape ls{0, 0};
+  cudaDeviceGetAttribute(&ls.sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ls.occ, kern, WARPS * 32, smem);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if (ls.occ < 1) ls.occ = 1;
+  std::lock_guard<std::mutex> lock(mu);
+  cache[key] = ls;
+  *out = ls;
+  return ADCT_OK;
+}
+
 template <class K, class P>
 adct_status launch_tma_kernel(K kern, const CUtensorMap& map, const P& params_in, int64_t tiles,
                               cudaStream_t stream, int stages = STAGES, int tile_bytes = TILE_BYTES) {
   P params = params_in;
   const int smem = WARPS * stages * tile_bytes + WARPS * stages * 8;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return cuda_fail(e);
-  int dev = 0, sms = 0, occ = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, smem);
-  if (e != cudaSuccess) return cuda_fail(e);
-  if (occ < 1) occ = 1;
-  int64_t grid = (int64_t)sms * occ;
+  LaunchShape ls;
+  adct_status st = launch_shape(reinterpret_cast<const void*>(kern), smem, &ls);
+  if (st) return st;
+  int64_t grid = (int64_t)ls.sms * ls.occ;
   // chunk = largest power of two <= 16 that still gives every resident warp >= 2 chunks
   int cshift = 4;
   while (cshift > 0 && (tiles >> cshift) < 2 * grid * WARPS) --cshift;
@@ -198,7 +230,7 @@ adct_status launch_tma_kernel(K kern, const CUtensorMap& map, const P& params_in
   if (grid < 1) grid = 1;
   kern<<<(unsigned)grid, WARPS * 32, smem, stream>>>(map, params);
   ++g_launches;
-  e = cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
 }
 
@@ -209,15 +241,10 @@ template <class K, class P>
 adct_status launch_tma2(K kern, const CUtensorMap& map, const CUtensorMap& omap, const P& params_in, int smem,
                         cudaStream_t stream) {
   P params = params_in;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return cuda_fail(e);
-  int dev = 0, sms = 0, occ = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, WARPS * 32, smem);
-  if (e != cudaSuccess) return cuda_fail(e);
-  if (occ < 1) occ = 1;
-  int64_t grid = (int64_t)sms * occ;
+  LaunchShape ls;
+  adct_status st = launch_shape(reinterpret_cast<const void*>(kern), smem, &ls);
+  if (st) return st;
+  int64_t grid = (int64_t)ls.sms * ls.occ;
   int cshift = 4;
   while (cshift > 0 && (params.tiles >> cshift) < 2 * grid * WARPS) --cshift;
   params.cshift = cshift;
@@ -227,7 +254,7 @@ adct_status launch_tma2(K kern, const CUtensorMap& map, const CUtensorMap& omap,
   if (grid < 1) grid = 1;
   kern<<<(unsigned)grid, WARPS * 32, smem, stream>>>(map, omap, params);
   ++g_launches;
-  e = cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
 }
 adct_status launch_forward_tma(adct_coef_t coef_t, const CUtensorMap& map, const CUtensorMap& omap,
