@@ -193,6 +193,15 @@ __device__ __forceinline__ void compress_fwd(const uint8_t* tile, int lane, uint
     pack_rows(lds64(tile + i * TILE_W + lane * 8), lds64(tile + (i + 8) * TILE_W + lane * 8), P[i]);
   fwd2d<BIAS2, RF>(P, Y);
 }
+// ... and the row pass H of the columns in SKIP (their column pass is skipped)
+template <int R, int SKIP>
+__device__ __forceinline__ void compress_fwd_h(const uint8_t* tile, int lane, uint32_t (&Y)[8][8], uint32_t (&H)[8][8]) {
+  uint32_t P[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    pack_rows(lds64(tile + i * TILE_W + lane * 8), lds64(tile + (i + 8) * TILE_W + lane * 8), P[i]);
+  fwd2d<BIAS2, R, SKIP>(P, Y, H);
+}
 
 // Inverse half: zonal weights / quantiser, inverse with C^T, error against the staged pixels.
 // Returns this lane's partial sum of squared errors (576 units for ZONAL) as an fp32 pair.
@@ -340,6 +349,50 @@ __device__ __forceinline__ float2 compress_resid(const uint32_t (&Y)[8][8], cons
   return f2add(f2add(s01, s23), f2add(s45, s67));
 }
 
+// Residual form with the fully discarded columns injected from the row pass (inverse2d_hc):
+// UH[L][i] = (576 / d_L) H[i][L], exact integers (< 2^18) — the same column-pass values as the
+// coefficient route, so every later node (and the exactness proof) is unchanged.
+#ifndef ADCT_RESID_HC
+#define ADCT_RESID_HC 1
+#endif
+template <int R>
+__device__ __forceinline__ float2 compress_resid_hc(const uint32_t (&Y)[8][8], const uint32_t (&H)[8][8],
+                                                    const CompressParams& p) {
+  constexpr int RM = RESID + R, HC = hcol_mask(R);
+  float2 V[64];
+  static_for<64>([&](auto KLc) {
+    constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
+    if constexpr (kept(RM, k, l) && !((HC >> l) & 1)) {
+      constexpr int c = wclass(k, l);
+      V[kl] = f2fma(biased_pair(Y[k][l]), f2(p.tab.wc[c]), f2(p.tab.cc[c]));  // W . (1 - M) . Y, exact
+    }
+  });
+  float2 UH[8][8];
+  static_for<8>([&](auto Lc) {
+    constexpr int L = decltype(Lc)::value;
+    if constexpr ((HC >> L) & 1) {
+      constexpr float wl = (float)(576 / dval(L));
+#pragma unroll
+      for (int i = 0; i < 8; ++i)  // + 0x80008000: both 16-bit lanes biased (the low lane's borrow cancels)
+        UH[L][i] = f2fma(biased_pair(H[i][L] + BIAS2), f2(wl), f2(-KF * wl));
+    }
+  });
+  float2 acc[8];
+#pragma unroll
+  for (int n = 0; n < 8; ++n) acc[n] = f2(0.f);
+  auto sq_row = [&](auto Ic, auto row) {
+    using cuda::std::get;
+    static_for<8>([&](auto Nc) {
+      constexpr int N = decltype(Nc)::value;
+      acc[N] = sqacc(get<N>(row), acc[N]);
+    });
+  };
+  inverse2d_hc<RM, HC>(V, UH, sq_row);
+  const float2 s01 = f2add(acc[0], acc[1]), s23 = f2add(acc[2], acc[3]);
+  const float2 s45 = f2add(acc[4], acc[5]), s67 = f2add(acc[6], acc[7]);
+  return f2add(f2add(s01, s23), f2add(s45, s67));
+}
+
 // Residual form of the quantiser error (compile-time r = 64, SSE only; C4's case).  By the same
 // orthogonality, x - x^ = C^T (Z - Z^) C: the kernel inverts the per-coefficient quantisation
 // residual instead of forming x^ and subtracting it from the re-read pixels.  With
@@ -465,8 +518,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     uint32_t Y[8][8];
     float2 e2;
     if constexpr (RES) {
-      compress_fwd<RESID + R, MODE>(tile, lane, Y);
-      e2 = compress_resid<R, GRP>(Y, p);
+      if constexpr (ADCT_RESID_HC && hcol_mask(R) != 0 && !GRP) {
+        uint32_t H[8][8];
+        compress_fwd_h<RESID + R, hcol_mask(R)>(tile, lane, Y, H);
+        e2 = compress_resid_hc<R>(Y, H, p);
+      } else {
+        compress_fwd<RESID + R, MODE>(tile, lane, Y);
+        e2 = compress_resid<R, GRP>(Y, p);
+      }
     } else if constexpr (MODE == MODE_QUANT && RECON == REC_NONE && R == 64) {
       compress_fwd<64, MODE>(tile, lane, Y);
       e2 = compress_quant_resid(Y, p);

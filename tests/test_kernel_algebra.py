@@ -83,3 +83,23 @@ def test_band_chain_equals_error_per_r():
         A_, c = _forms(e)
         assert np.array_equal(A_, 576 * np.eye(64, dtype=np.int64) - _affine_R(r)), r
         assert np.all(c == 0)
+
+
+@pytest.mark.parametrize("L", list(range(8)))
+def test_fully_discarded_column_identity(L):
+    # compress_resid_hc: a column whose coefficients the mask discards entirely contributes
+    # C0^T diag(W[:, L]) C0 H[:, L] = (576 / d_L) H[:, L] to the column pass (H = row pass of the pixels)
+    T, W = EB.T, EB.W
+    d = np.diag(T @ T.T)
+    assert np.array_equal(T.T @ np.diag(W[:, L]) @ T, (576 // d[L]) * np.eye(8, dtype=np.int64))
+    assert 576 % d[L] == 0
+
+
+@pytest.mark.parametrize("r", list(range(1, 64)))
+def test_hcol_columns_are_exactly_the_empty_ones(r):
+    # the kernel injects column L iff no zig-zag index < r lies in it (hcol_mask)
+    M = np.array([[EB.zz(i, j) < r for j in range(8)] for i in range(8)])
+    empty = [L for L in range(8) if not M[:, L].any()]
+    # for the residual kernels (r >= 24) these are the columns 7 (r <= 28) and 6 (r <= 27)
+    if r >= 24:
+        assert empty == [L for L in (6, 7) if (L == 7 and r <= 28) or (L == 6 and r <= 27)]
