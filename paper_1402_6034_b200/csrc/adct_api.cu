@@ -6,6 +6,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <utility>
 #include "adct_kernels.cuh"
 
 namespace adct {
@@ -198,8 +199,18 @@ adct_status launch_shape(const void* kern, int smem, LaunchShape* out) {
       return ADCT_OK;
     }
   }
-  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return cuda_fail(e);
+  {
+    // the attribute is a per-kernel maximum: raise it only, so a later launch of the same kernel
+    // with a smaller shared-memory size cannot invalidate a cached larger one
+    static std::map<std::pair<const void*, int>, int> attr_max;
+    std::lock_guard<std::mutex> lock(mu);
+    int& cur = attr_max[std::make_pair(kern, dev)];
+    if (smem > cur) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return cuda_fail(e);
+      cur = smem;
+    }
+  }
   LaunchShape ls{0, 0};
   cudaDeviceGetAttribute(&ls.sms, cudaDevAttrMultiProcessorCount, dev);
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ls.occ, kern, WARPS * 32, smem);
