@@ -323,6 +323,23 @@ def test_cuda_graph_capture_and_replay():
 
 # ------------------------------------------------------------------ fused compress (quantiser)
 
+@pytest.mark.parametrize("q", [16.0, 5.0])
+def test_compress_quant_u8_recon_vs_oracle(q):
+    """Quantiser + u8 reconstruction: clamp(round_half_away(x^)) of the fp32 x^ against the oracle's
+    float64 x^ — identical except where x^ lies within the fp32 reconstruction error (R15: 6.6e-5,
+    bar 1e-4) of a rounding boundary k + 0.5, and there by at most one step; both paths tested
+    (bulk-store path w % 16 == 0, per-lane path otherwise)."""
+    for w in (96, 264):
+        imgs = np.concatenate([S.corpus_c2(3, 64, w), rng.integers(0, 256, (2, 64, w), dtype=np.uint8)])
+        want_f = O.reconstruct_quant(imgs, q)
+        want = O.round_u8(want_f)
+        _, rec8 = A.compress_psnr(dev(imgs), 64, q=q, recon="u8")
+        got = host(rec8).astype(np.int64)
+        diff = np.abs(got - want.astype(np.int64))
+        near = np.abs(np.abs(want_f - np.floor(want_f)) - 0.5) < 1e-4
+        assert diff.max() <= 1
+        assert np.all(near[diff > 0]), (w, int((diff > 0).sum()))
+
 @pytest.mark.parametrize("q", [16.0, 5.0, 3.0])
 def test_compress_quant_vs_oracle(q):
     imgs = np.concatenate([S.corpus_c2(3, 64, 64), rng.integers(0, 256, (2, 64, 64), dtype=np.uint8)])
