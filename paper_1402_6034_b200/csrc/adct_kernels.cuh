@@ -483,8 +483,11 @@ constexpr bool compress_grouped(int R) { return ADCT_GROUPED || (R >= 11 && R < 
 #define ADCT_MINB_RT 2  // measured: 5-17 % faster than 3 (no spills), profiles/r01_variants_session3.txt
 #endif
 // measured on B200 (profiles/r01_tune_minb.txt): small r wants occupancy, mid r registers
+#ifndef ADCT_MINB_RESID
+#define ADCT_MINB_RESID 4
+#endif
 constexpr int compress_minb(int R) {
-  return compress_resid_r(R) ? 4 : (R == 1 ? 6 : 4);
+  return compress_resid_r(R) ? ADCT_MINB_RESID : (R == 1 ? 6 : 4);
 }
 
 template <int R, int MODE, int RECON, int ST = compress_stages(R),
