@@ -388,25 +388,33 @@ adct_status adct_inverse(const void* coef, adct_coef_t coef_t, int64_t n, int64_
       p.tab.c[k * 8 + l] = make_float2(-KF * m, -KF * m);  // TMA int16 path: debias of the magic pair
     }
   cudaStream_t s0 = (cudaStream_t)stream;
-  if (coef_t == ADCT_COEF_I16) {  // staged by TMA through the warp rings (HBM-bound path)
-    CUtensorMap map;
-    if ((st = make_i16_map(&map, coef, n, h, w, coef_pitch, coef_img_stride))) return st;
 #ifndef ADCT_INV_TMA_STORE
 #define ADCT_INV_TMA_STORE 1
 #endif
-    // reconstruction tiles leave through shared memory + TMA bulk stores.  Measured on B200: a bulk
-    // tensor store writes a row's last partial 16-byte chunk whole, so the u8 plane takes this path
-    // only when w is a multiple of 16 (tests/test_gpu_parity.py::test_no_writes_outside_outputs)
-    if (ADCT_INV_TMA_STORE && (dst_t == ADCT_RECON_F32 || (w & 15) == 0)) {
-      CUtensorMap omap;
-      if (dst_t == ADCT_RECON_F32) {
-        if ((st = make_plane_map(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, dst, n, h, w, dst_pitch, dst_img_stride)))
-          return st;
-        return launch_tma2(k_inverse_i16_tma<REC_F32>, map, omap, p, invt_smem_bytes(REC_F32), s0);
-      }
-      if ((st = make_u8_map(&omap, (const uint8_t*)dst, n, h, w, dst_pitch, dst_img_stride))) return st;
-      return launch_tma2(k_inverse_i16_tma<REC_U8>, map, omap, p, invt_smem_bytes(REC_U8), s0);
-    }
+  // coefficient tiles in through the TMA rings, reconstruction tiles out through shared memory +
+  // TMA bulk stores.  Measured on B200: a bulk tensor store writes a row's last partial 16-byte
+  // chunk whole, so the u8 plane takes this path only when w is a multiple of 16
+  // (tests/test_gpu_parity.py::test_no_writes_outside_outputs)
+  if (ADCT_INV_TMA_STORE && (dst_t == ADCT_RECON_F32 || (w & 15) == 0)) {
+    CUtensorMap map, omap;
+    const CUtensorMapDataType it = coef_t == ADCT_COEF_I16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                   : coef_t == ADCT_COEF_I32 ? CU_TENSOR_MAP_DATA_TYPE_INT32
+                                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    if ((st = make_plane_map(&map, it, coef, n, h, w, coef_pitch, coef_img_stride))) return st;
+    if (dst_t == ADCT_RECON_F32)
+      st = make_plane_map(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, dst, n, h, w, dst_pitch, dst_img_stride);
+    else
+      st = make_u8_map(&omap, (const uint8_t*)dst, n, h, w, dst_pitch, dst_img_stride);
+    if (st) return st;
+#define ADCT_INVT(IN, RC) launch_tma2(k_inverse_tma<IN, RC>, map, omap, p, invt_smem_bytes(IN, RC), s0)
+    if (coef_t == ADCT_COEF_I16) return dst_t == ADCT_RECON_F32 ? ADCT_INVT(OUT_I16, REC_F32) : ADCT_INVT(OUT_I16, REC_U8);
+    if (coef_t == ADCT_COEF_I32) return dst_t == ADCT_RECON_F32 ? ADCT_INVT(OUT_I32, REC_F32) : ADCT_INVT(OUT_I32, REC_U8);
+    return dst_t == ADCT_RECON_F32 ? ADCT_INVT(OUT_F32, REC_F32) : ADCT_INVT(OUT_F32, REC_U8);
+#undef ADCT_INVT
+  }
+  if (coef_t == ADCT_COEF_I16) {  // u8 planes with w % 16 != 0: TMA ring in, per-lane stores out
+    CUtensorMap map;
+    if ((st = make_i16_map(&map, coef, n, h, w, coef_pitch, coef_img_stride))) return st;
     return dst_t == ADCT_RECON_F32
                ? launch_tma_kernel(k_inverse_i16<REC_F32>, map, p, p.tiles, s0, 2, 2 * TILE_BYTES)
                : launch_tma_kernel(k_inverse_i16<REC_U8>, map, p, p.tiles, s0, 2, 2 * TILE_BYTES);

@@ -911,14 +911,19 @@ __global__ void __launch_bounds__(WARPS * 32, 3)
 #define ADCT_INVT_MINB 1
 #endif
 constexpr int invt_stage_bytes(int RECON) { return RECON == REC_F32 ? 4 * TILE_BYTES : TILE_BYTES; }
-constexpr int invt_smem_bytes(int RECON) {
-  return WARPS * 2 * (2 * TILE_BYTES) + FWDT_BAR_BYTES + WARPS * invt_stage_bytes(RECON);
+constexpr int invt_in_bytes(int IN) { return IN == OUT_I16 ? 2 * TILE_BYTES : 4 * TILE_BYTES; }
+constexpr int invt_smem_bytes(int IN, int RECON) {
+  return WARPS * 2 * invt_in_bytes(IN) + FWDT_BAR_BYTES + WARPS * invt_stage_bytes(RECON);
 }
-template <int RECON>
+// int16 / int32 / f32 coefficient planes in (TMA ring of 8 / 16 / 16 KiB tiles), reconstruction out
+// through shared-memory staging + one TMA bulk-tensor store per tile.  Coefficients enter the f32x2
+// inverse weighted by the runtime mask table: int16 through the biased-pair magic, int32 through
+// the 1.5 * 2^23 magic (exact for |Y| < 2^22), f32 (Z) directly.
+template <int IN, int RECON>
 __global__ void __launch_bounds__(WARPS * 32, ADCT_INVT_MINB)
-    k_inverse_i16_tma(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
-                      const __grid_constant__ InverseParams p) {
-  constexpr int TB = 2 * TILE_BYTES;
+    k_inverse_tma(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
+                  const __grid_constant__ InverseParams p) {
+  constexpr int TB = invt_in_bytes(IN);
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   uint8_t* ring = smem + warp * (2 * TB);
@@ -930,17 +935,34 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INVT_MINB)
     float2 V[64];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const uint4 a = *reinterpret_cast<const uint4*>(tile + (k * TILE_W + lane * 8) * 2);
-      const uint4 b = *reinterpret_cast<const uint4*>(tile + ((k + 8) * TILE_W + lane * 8) * 2);
-      const uint32_t wa[4] = {a.x ^ 0x80008000u, a.y ^ 0x80008000u, a.z ^ 0x80008000u, a.w ^ 0x80008000u};
-      const uint32_t wb[4] = {b.x ^ 0x80008000u, b.y ^ 0x80008000u, b.z ^ 0x80008000u, b.w ^ 0x80008000u};
+      if constexpr (IN == OUT_I16) {
+        const uint4 a = *reinterpret_cast<const uint4*>(tile + (k * TILE_W + lane * 8) * 2);
+        const uint4 b = *reinterpret_cast<const uint4*>(tile + ((k + 8) * TILE_W + lane * 8) * 2);
+        const uint32_t wa[4] = {a.x ^ 0x80008000u, a.y ^ 0x80008000u, a.z ^ 0x80008000u, a.w ^ 0x80008000u};
+        const uint32_t wb[4] = {b.x ^ 0x80008000u, b.y ^ 0x80008000u, b.z ^ 0x80008000u, b.w ^ 0x80008000u};
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
+        for (int m = 0; m < 4; ++m) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int kl = k * 8 + 2 * m + h;
-          const uint32_t P = __byte_perm(wa[m], wb[m], h ? 0x7632 : 0x5410);  // (A + 2^15) | (B + 2^15) << 16
-          V[kl] = f2fma(biased_pair(P), f2(p.tab.w[kl].x), f2(p.tab.c[kl].x));  // w Y (0 if masked)
+          for (int h = 0; h < 2; ++h) {
+            const int kl = k * 8 + 2 * m + h;
+            const uint32_t P = __byte_perm(wa[m], wb[m], h ? 0x7632 : 0x5410);  // (A + 2^15) | (B + 2^15) << 16
+            V[kl] = f2fma(biased_pair(P), f2(p.tab.w[kl].x), f2(p.tab.c[kl].x));  // w Y (0 if masked)
+          }
+        }
+      } else {
+        const uint4* ra = reinterpret_cast<const uint4*>(tile + (k * TILE_W + lane * 8) * 4);
+        const uint4* rb = reinterpret_cast<const uint4*>(tile + ((k + 8) * TILE_W + lane * 8) * 4);
+        const uint4 a0 = ra[0], a1 = ra[1], b0 = rb[0], b1 = rb[1];
+        const uint32_t av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const uint32_t bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+          const int kl = k * 8 + l;
+          if constexpr (IN == OUT_I32)  // 1.5 * 2^23 + Y as a float, then w Y in one FFMA2 (exact)
+            V[kl] = f2fma(make_float2(__uint_as_float(av[l] + 0x4B400000u), __uint_as_float(bv[l] + 0x4B400000u)),
+                          f2(p.tab.w[kl].x), f2(-12582912.0f * p.tab.w[kl].x));
+          else
+            V[kl] = __fmul2_rn(make_float2(__uint_as_float(av[l]), __uint_as_float(bv[l])), p.tab.w[kl]);
         }
       }
     }
