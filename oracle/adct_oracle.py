@@ -31,6 +31,7 @@ __all__ = [
     "coarse_matrix", "frobenius_optimal_scale", "sdct_matrix", "transfer_error_energy",
     "zigzag_order", "zigzag_index", "zonal_mask", "to_blocks", "from_blocks",
     "forward_int", "forward_scaled", "inverse", "reconstruct_zonal", "reconstruct_zonal_exact",
+    "reconstruct_from_coef_exact", "round_u8_exact576",
     "quantize_exact", "reconstruct_quant", "sse_per_image", "psnr", "mean_psnr",
     "compress_zonal_sse", "compress_zonal_sse576", "compress_quant_sse", "round_u8", "uqi", "ape",
 ]
@@ -235,6 +236,25 @@ def reconstruct_zonal_exact(img: np.ndarray, r: int) -> np.ndarray:
     return from_blocks(T.T @ V @ T)
 
 
+def reconstruct_from_coef_exact(Y: np.ndarray, r: int) -> np.ndarray:
+    """Exact-integer inverse of an arbitrary integer coefficient plane Y (image-shaped, R12):
+    R = C0^T (W . M_r . Y) C0 per block (int64), so the reconstruction is R / 576 exactly — the
+    inverse procedure with C^T and S folded into integer weights, the same
+    composition as reconstruct_zonal_exact but from given coefficients instead of a forward."""
+    T = c0_matrix()
+    d = np.diag(T @ T.T)
+    W = 576 // np.outer(d, d)
+    V = to_blocks(np.asarray(Y)).astype(np.int64) * (W * zonal_mask(r))
+    return from_blocks(T.T @ V @ T)
+
+
+def round_u8_exact576(R: np.ndarray) -> np.ndarray:
+    """clamp(round_half_away(R / 576), 0, 255) decided on the exact integer R (reading R3): for
+    R >= 0, floor((R + 288) / 576); every negative R clamps to 0."""
+    R = np.asarray(R, dtype=np.int64)
+    return np.clip(np.floor_divide(R + 288, 576), 0, 255).astype(np.uint8)
+
+
 def quantize_exact(Y: np.ndarray, q: float) -> np.ndarray:
     """k_ij = round_half_away(Z_ij / q) with Z_ij = Y_ij / sqrt(d_i d_j), decided EXACTLY.
 
@@ -275,10 +295,16 @@ def quantize_exact(Y: np.ndarray, q: float) -> np.ndarray:
     return from_blocks(np.sign(Yb) * k)
 
 
-def reconstruct_quant(img: np.ndarray, q: float) -> np.ndarray:
-    """Forward, D-scaled uniform quantiser (step q), dequantise Z_hat = q k, inverse C^T (R10). float64."""
+def reconstruct_quant(img: np.ndarray, q: float, r: int = 64) -> np.ndarray:
+    """Forward, D-scaled uniform quantiser (step q), dequantise Z_hat = q k, inverse C^T (R10). float64.
+
+    With r < 64 the zonal step is applied too: only the first r zig-zag coefficients are kept
+     and quantised, the others are discarded (k = 0) — S merged into the quantisation
+    step of the kept coefficients, reading R17."""
     C = proposed_matrix()
     k = quantize_exact(forward_int(img), q)
+    if r < 64:
+        k = _mask_image(k, r)
     return inverse(q * k.astype(np.float64), C)
 
 
@@ -331,12 +357,13 @@ def compress_zonal_sse576(img: np.ndarray, r: int) -> np.ndarray:
     return (e * e).reshape(img.shape[0], -1).sum(axis=1)
 
 
-def compress_quant_sse(img: np.ndarray, q: float) -> np.ndarray:
-    """Per-image SSE of the quantiser pipeline (R10) on the unrounded reconstruction (R3)."""
+def compress_quant_sse(img: np.ndarray, q: float, r: int = 64) -> np.ndarray:
+    """Per-image SSE of the quantiser pipeline (R10; zonal r as in reconstruct_quant, R17) on the
+    unrounded reconstruction (R3)."""
     img = np.asarray(img)
     if img.ndim == 2:
         img = img[None]
-    return sse_per_image(img, reconstruct_quant(img, q))
+    return sse_per_image(img, reconstruct_quant(img, q, r))
 
 
 # --------------------------------------------------------------------------------------

@@ -386,6 +386,7 @@ adct_status adct_inverse(const void* coef, adct_coef_t coef_t, int64_t n, int64_
         m = (coef_t == ADCT_COEF_F32) ? (float)(576.0 / sqrt(dd_host(k, l))) : (float)wval(k, l);
       p.tab.w[k * 8 + l] = make_float2(m, m);
       p.tab.c[k * 8 + l] = make_float2(-KF * m, -KF * m);  // TMA int16 path: debias of the magic pair
+      p.tab.keep[k * 8 + l] = zz_host(k, l) < r ? 0xFFFFFFFFu : 0u;
     }
   cudaStream_t s0 = (cudaStream_t)stream;
 #ifndef ADCT_INV_TMA_STORE

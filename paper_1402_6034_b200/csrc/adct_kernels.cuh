@@ -32,6 +32,7 @@ struct Tables {
   float cc[8];   // ZONAL compile-time r: -KF * W per weight class
   float2 w[64];  // ZONAL: (W, W); QUANT: q / sqrt(d_k d_l); INVERSE: per-coef scale — 0 where masked
   float2 c[64];  // ZONAL: (-KF W, -KF W) [masked: 0]; QUANT: (c', c') quantiser reciprocal
+  uint32_t keep[64];  // INVERSE: all ones where the zonal mask keeps the coefficient, else 0
   float sq[8];   // QUANT residual form: 1 / (q sqrt dd) per weight class as hi + lo fp32 pair
   float sql[8];
   float qscale;  // QUANT residual form: SSE = (q / 8)^2 * sum of the weighted inverse's squares
@@ -84,27 +85,46 @@ struct InverseParams {
 // u8 reconstruction of one output row of both blocks, x[n] = (A, B) pair of pixel n.
 // S576: u8 = clamp(round_half_away(R / 576)) = clamp(floor((R + 288.5) / 576)) for integer R
 // (never within 8.7e-4 of an integer, so the fp32 product is floored exactly); else clamp(floor(x^ + 0.5)).
-// One FADD2 + one round-toward-zero FFMA2 with the magic 2^23 + 512 per pixel pair puts
-// floor(y) + 512 in the low 16 bits; two halves pack into one word, clamp to [512, 767] with
-// VIMNMX.U16x2, and the low bytes are floor(y) clamped to [0, 255].
-template <bool S576>
+// Fast form (SAFE = false): one FADD2 + one round-toward-zero FFMA2 with the magic 2^23 + 512 per pixel
+// pair puts floor(y) + 512 in the low 16 bits; two halves pack into one word, clamp to [512, 767] with
+// VIMNMX.U16x2, and the low bytes are floor(y) clamped to [0, 255].  The magic holds only for
+// floor(y) in [-512, 65023]: the fused zonal compress uses it because its R is proven inside
+// [-182325, 329205] (y in [-316, 572], tools/exactness_bounds.py).
+// SAFE = true (quantiser reconstruction, inverse from arbitrary coefficient planes): y is first
+// saturated to [0, 256] / 256 by one scalar FFMA.SAT per value (NaN -> 0), z = sat((y + 0.5) / 256),
+// then floor(256 z) + 512 by the same round-toward-zero FFMA2 — every input clamps correctly.
+// For S576 the scaled sum RN(R / 147456 + 288.5 / 147456) is within 3e-5 (in pixel units) of
+// (R + 288.5) / 576 for every R that does not saturate, far inside the 8.7e-4 margin.
+// u8 rounding kinds: exact-integer R = 576 x^ (fast magic / saturating), real R = 576 x^ (from an f32
+// coefficient plane: round_half_away(R / 576) with no integer offset), real x^ (quantiser).
+enum { U8_FAST576 = 0, U8_SAFE576 = 1, U8_SAFE576R = 2, U8_SAFEX = 3 };
+template <int U8K>
 __device__ __forceinline__ void u8_rows(const float2 (&x)[8], uint2& ra, uint2& rb) {
+  constexpr bool SAFE = U8K == U8_SAFE576 || U8K == U8_SAFE576R || U8K == U8_SAFEX;
+  constexpr bool S576 = U8K == U8_FAST576 || U8K == U8_SAFE576 || U8K == U8_SAFE576R;
   uint32_t ta[8], tb[8];
 #pragma unroll
   for (int n = 0; n < 8; ++n) {
     float2 t;
-    if constexpr (S576) {
+    if constexpr (SAFE) {
+      constexpr float c1 = S576 ? (float)(1.0 / 147456.0) : 0.00390625f;
+      constexpr float c2 = U8K == U8_SAFE576 ? (float)(288.5 / 147456.0) : 0.001953125f;
+      float za, zb;
+      asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(za) : "f"(x[n].x), "f"(c1), "f"(c2));
+      asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(zb) : "f"(x[n].y), "f"(c1), "f"(c2));
+      const float2 z = make_float2(za, zb);
+      unsigned long long d;
+      asm("fma.rz.f32x2 %0, %1, %2, %3;" : "=l"(d)
+          : "l"(*reinterpret_cast<const unsigned long long*>(&z)), "l"(0x4380000043800000ull),
+            "l"(0x4B0002004B000200ull));
+      t = *reinterpret_cast<float2*>(&d);
+    } else {
+      static_assert(U8K == U8_FAST576, "fast form: exact-integer R only");
       const float2 sft = f2add(x[n], f2(288.5f));  // exact: R is an integer below 2^19
       unsigned long long d;
       asm("fma.rz.f32x2 %0, %1, %2, %3;" : "=l"(d)
           : "l"(*reinterpret_cast<const unsigned long long*>(&sft)), "l"(0x3AE38E393AE38E39ull),
             "l"(0x4B0002004B000200ull));
-      t = *reinterpret_cast<float2*>(&d);
-    } else {
-      const float2 y = f2add(x[n], f2(0.5f));
-      unsigned long long d;
-      asm("add.rz.f32x2 %0, %1, %2;" : "=l"(d)
-          : "l"(*reinterpret_cast<const unsigned long long*>(&y)), "l"(0x4B0002004B000200ull));
       t = *reinterpret_cast<float2*>(&d);
     }
     ta[n] = __float_as_uint(t.x);
@@ -124,7 +144,7 @@ __device__ __forceinline__ void u8_rows(const float2 (&x)[8], uint2& ra, uint2& 
   rb = make_uint2(__byte_perm(pb[0], pb[1], 0x6420), __byte_perm(pb[2], pb[3], 0x6420));
 }
 
-template <int RECON, bool S576>
+template <int RECON, bool S576, int U8K>
 __device__ __forceinline__ void store_recon_row(uint8_t* base, int64_t pitch, int h, int w, int row_a,
                                                 int col, const float2 (&x)[8]) {
   // S576: x[n] = (R_A[n], R_B[n]) with R = 576 x^ exactly (integers in fp32); else x[n] = x^ itself
@@ -146,7 +166,7 @@ __device__ __forceinline__ void store_recon_row(uint8_t* base, int64_t pitch, in
   }
   if constexpr (RECON == REC_U8) {
     uint2 ra, rb;
-    u8_rows<S576>(x, ra, rb);
+    u8_rows<U8K>(x, ra, rb);
     *reinterpret_cast<uint2*>(base + (int64_t)row_a * pitch + col) = ra;
     if (row_a + 8 < h) *reinterpret_cast<uint2*>(base + (int64_t)(row_a + 8) * pitch + col) = rb;
   }
@@ -154,7 +174,7 @@ __device__ __forceinline__ void store_recon_row(uint8_t* base, int64_t pitch, in
 
 // The same two output rows into a warp-private shared-memory staging tile laid out as the 16 x 256
 // box of a TMA bulk-tensor store (f32: 1 KiB per row, u8: 256 B per row).
-template <int RECON, bool S576>
+template <int RECON, bool S576, int U8K>
 __device__ __forceinline__ void stage_recon_row(uint8_t* buf, int row_a, int lane, const float2 (&x)[8]) {
 #pragma unroll
   for (int b = 0; b < 2; ++b) {
@@ -170,7 +190,7 @@ __device__ __forceinline__ void stage_recon_row(uint8_t* buf, int row_a, int lan
   }
   if constexpr (RECON == REC_U8) {
     uint2 ra, rb;
-    u8_rows<S576>(x, ra, rb);
+    u8_rows<U8K>(x, ra, rb);
     *reinterpret_cast<uint2*>(buf + row_a * TILE_W + lane * 8) = ra;
     *reinterpret_cast<uint2*>(buf + (row_a + 8) * TILE_W + lane * 8) = rb;
   }
@@ -303,9 +323,9 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
         if constexpr (RECON != REC_NONE) xr[N] = val(get<N>(row));
       }
     });
-    if constexpr (RECON != REC_NONE && STAGE) stage_recon_row<RECON, (MODE == MODE_ZONAL)>(sbuf, I, lane, xr);
+    if constexpr (RECON != REC_NONE && STAGE) stage_recon_row<RECON, (MODE == MODE_ZONAL), (MODE == MODE_ZONAL ? U8_FAST576 : U8_SAFEX)>(sbuf, I, lane, xr);
     else if constexpr (RECON != REC_NONE)
-      store_recon_row<RECON, (MODE == MODE_ZONAL)>(rbase, p.recon_pitch, p.h, p.w, ty * TILE_H + I, col, xr);
+      store_recon_row<RECON, (MODE == MODE_ZONAL), (MODE == MODE_ZONAL ? U8_FAST576 : U8_SAFEX)>(rbase, p.recon_pitch, p.h, p.w, ty * TILE_H + I, col, xr);
   };
   if constexpr (GROUPED) inverse2d_grouped<RF>(V, err_row);
   else inverse2d<RF>(V, err_row);
@@ -841,7 +861,11 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_inverse(const __grid_constant
       load_coef_row<IN>(base + (int64_t)ra * p.coef_pitch, cok && ra < p.h, a);
       load_coef_row<IN>(base + (int64_t)rb * p.coef_pitch, cok && rb < p.h, b);
 #pragma unroll
-      for (int l = 0; l < 8; ++l) V[k * 8 + l] = __fmul2_rn(make_float2(a[l], b[l]), p.tab.w[k * 8 + l]);
+      for (int l = 0; l < 8; ++l) {
+        const uint32_t km = p.tab.keep[k * 8 + l];  // masked f32 NaN / Inf must not reach the block
+        V[k * 8 + l] = __fmul2_rn(make_float2(__uint_as_float(__float_as_uint(a[l]) & km),
+                                              __uint_as_float(__float_as_uint(b[l]) & km)), p.tab.w[k * 8 + l]);
+      }
     }
     uint8_t* dbase = p.dst + (int64_t)img * p.dst_img_stride;
     inverse2d<RT>(V, [&](auto Ic, auto row) {
@@ -851,7 +875,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_inverse(const __grid_constant
         constexpr int N = decltype(Nc)::value;
         xr[N] = val(cuda::std::get<N>(row));
       });
-      store_recon_row<RECON, true>(dbase, p.dst_pitch, p.h, p.w, ty * TILE_H + I, col, xr);
+      store_recon_row<RECON, true, (IN == OUT_F32 ? U8_SAFE576R : U8_SAFE576)>(dbase, p.dst_pitch, p.h, p.w, ty * TILE_H + I, col, xr);
     });
   }
 }
@@ -897,13 +921,14 @@ __global__ void __launch_bounds__(WARPS * 32, 3)
         constexpr int N = decltype(Nc)::value;
         xr[N] = val(cuda::std::get<N>(row));
       });
-      store_recon_row<RECON, true>(dbase, p.dst_pitch, p.h, p.w, ty * TILE_H + I, col, xr);
+      store_recon_row<RECON, true, U8_SAFE576>(dbase, p.dst_pitch, p.h, p.w, ty * TILE_H + I, col, xr);
     });
   });
 }
 
 // ------------------------------------------------------------------------------------------
-// Inverse from an int16 plane with TMA bulk-tensor stores of the reconstruction: the warp's
+// k_inverse_tma<IN, RECON>: inverse from an int16 / int32 / f32 coefficient plane with TMA bulk-tensor
+// stores of the reconstruction: the warp's
 // 16 x 256 output tile (f32: 16 KiB, u8: 4 KiB) is staged in shared memory row by row and stored
 // by one elected lane; the staging buffer is rewritten only after the previous store has read it.
 // ------------------------------------------------------------------------------------------
@@ -918,7 +943,7 @@ constexpr int invt_smem_bytes(int IN, int RECON) {
 // int16 / int32 / f32 coefficient planes in (TMA ring of 8 / 16 / 16 KiB tiles), reconstruction out
 // through shared-memory staging + one TMA bulk-tensor store per tile.  Coefficients enter the f32x2
 // inverse weighted by the runtime mask table: int16 through the biased-pair magic, int32 through
-// the 1.5 * 2^23 magic (exact for |Y| < 2^22), f32 (Z) directly.
+// an exact I2FP conversion (any int32), f32 (Z) directly with masked positions zeroed by their bits.
 template <int IN, int RECON>
 __global__ void __launch_bounds__(WARPS * 32, ADCT_INVT_MINB)
     k_inverse_tma(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
@@ -958,11 +983,11 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INVT_MINB)
 #pragma unroll
         for (int l = 0; l < 8; ++l) {
           const int kl = k * 8 + l;
-          if constexpr (IN == OUT_I32)  // 1.5 * 2^23 + Y as a float, then w Y in one FFMA2 (exact)
-            V[kl] = f2fma(make_float2(__uint_as_float(av[l] + 0x4B400000u), __uint_as_float(bv[l] + 0x4B400000u)),
-                          f2(p.tab.w[kl].x), f2(-12582912.0f * p.tab.w[kl].x));
-          else
-            V[kl] = __fmul2_rn(make_float2(__uint_as_float(av[l]), __uint_as_float(bv[l])), p.tab.w[kl]);
+          if constexpr (IN == OUT_I32)  // exact int -> f32 conversion (I2FP) for any int32, then w Y
+            V[kl] = __fmul2_rn(make_float2((float)(int)av[l], (float)(int)bv[l]), p.tab.w[kl]);
+          else  // a masked position is zeroed by its bits (a NaN / Inf there must not reach the block)
+            V[kl] = __fmul2_rn(make_float2(__uint_as_float(av[l] & p.tab.keep[kl]), __uint_as_float(bv[l] & p.tab.keep[kl])),
+                               p.tab.w[kl]);
         }
       }
     }
@@ -975,7 +1000,7 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INVT_MINB)
         constexpr int N = decltype(Nc)::value;
         xr[N] = val(cuda::std::get<N>(row));
       });
-      stage_recon_row<RECON, true>(buf, I, lane, xr);
+      stage_recon_row<RECON, true, (IN == OUT_F32 ? U8_SAFE576R : U8_SAFE576)>(buf, I, lane, xr);
     });
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();

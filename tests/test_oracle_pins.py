@@ -56,7 +56,10 @@ def test_P3_proposed_is_orthogonal():
 def test_c0_is_not_orthogonal_and_coarse():
     T = O.c0_matrix().astype(float)
     assert np.abs(np.linalg.inv(T) - T.T).max() > 0.5        # P:180-181 C0^-1 != C0^T
-    assert np.allclose(O.coarse_matrix(), 0.5 * T)
+    # P:160-164 "C_hat = 1/2 C0", pinned against the displayed C0 (golden), not the oracle's own C0
+    assert np.array_equal(2.0 * O.coarse_matrix(), golden_c0().astype(float))
+    # and its rows all have the same norm only where C0's rows do: ||row||^2 = d / 4
+    assert np.allclose((O.coarse_matrix() ** 2).sum(axis=1), np.array([8, 6, 4, 6, 8, 6, 4, 6]) / 4.0)
 
 
 def test_P4_frobenius_scale_0_3922():
@@ -322,6 +325,79 @@ def test_P14_quantizer_exact_vs_decimal_brute_force():
                 assert kk == want, (q, i, j, y, kk, want)
 
 
+def _reachable_y_range(i, j):
+    """[lo, hi] of Y_ij = sum_mn T_im T_jn x_mn over all uint8 blocks (every integer in between is
+    reachable: the outer-product entries are in {0, +-1})."""
+    T = golden_c0()
+    P = np.outer(T[i], T[j])
+    return int(255 * P[P < 0].sum()), int(255 * P[P > 0].sum())
+
+
+@pytest.mark.parametrize("q", [16.0])
+def test_P14_quantizer_full_reachable_domain(q):
+    """P14 on the whole input domain: for every position (i, j) and every reachable Y_ij, the oracle's exact decision equals round_half_away(Y / (q sqrt(d_i d_j)))
+    recomputed with 60-digit decimal arithmetic (Decimal ROUND_HALF_UP = ties away from zero).
+    The domain is every reachable Y at every position (587,584 pairs)."""
+    from decimal import Decimal, ROUND_HALF_UP, getcontext
+    getcontext().prec = 60
+    d = [8, 6, 4, 6, 8, 6, 4, 6]
+    total = 0
+    memo = {}
+    for i in range(8):
+        for j in range(8):
+            lo, hi = _reachable_y_range(i, j)
+            Ys = np.arange(lo, hi + 1)
+            total += len(Ys)
+            Y = np.zeros((len(Ys), 8, 8), dtype=np.int64)
+            Y[:, i, j] = Ys
+            k = O.to_blocks(O.quantize_exact(O.from_blocks(Y[:, None, None]), q))[:, 0, 0, i, j]
+            dd = d[i] * d[j]
+            if dd not in memo:
+                den = Decimal(q) * Decimal(dd).sqrt()
+                yall = np.arange(-16320, 16321)
+                memo[dd] = dict(zip(yall.tolist(), [int((Decimal(y) / den).quantize(Decimal(1), rounding=ROUND_HALF_UP))
+                                                    for y in yall.tolist()]))
+            want = np.array([memo[dd][y] for y in Ys.tolist()])
+            bad = np.nonzero(k != want)[0]
+            assert len(bad) == 0, (i, j, Ys[bad[:5]], k[bad[:5]], want[bad[:5]])
+    # 587,584 reachable (position, Y) pairs (SURVEY §8(c) quotes 620,224 for a looser per-position range;
+    # every integer between the exact extremes of sum_mn T_im T_jn x_mn is reachable and is covered here)
+    assert total == 587584
+
+
+def test_quant_zonal_r_parseval_identity():
+    """Reading R17 (quantiser with zonal r): by the orthogonality of C the pixel-domain SSE of
+    C^T (q M_r k) C equals the coefficient-domain energy sum_kept (Z - q k)^2 + sum_discarded Z^2, an
+    identity the oracle's literal inverse must satisfy for every r (a dropped mask, a wrong index or a
+    transposed operand in the composition breaks it)."""
+    imgs = np.concatenate([S.corpus_c2(3, 32, 48), rng.integers(0, 256, (2, 32, 48), dtype=np.uint8)])
+    Zb = O.to_blocks(O.forward_scaled(imgs))
+    for q in (16.0, 5.0, 350.0):
+        kb = O.to_blocks(O.quantize_exact(O.forward_int(imgs), q)).astype(np.float64)
+        for r in (1, 2, 10, 36, 63, 64):
+            M = O.zonal_mask(r)
+            want = (np.where(M, Zb - q * kb, Zb) ** 2).sum(axis=(1, 2, 3, 4))
+            got = O.compress_quant_sse(imgs, q, r)
+            assert np.allclose(got, want, rtol=1e-9, atol=1e-6), (q, r)
+    assert np.array_equal(O.reconstruct_quant(imgs, 16.0, 64), O.reconstruct_quant(imgs, 16.0))
+
+
+def test_quant_zonal_r_limits():
+    """Tiny step: the quantised zonal reconstruction tends to the plain zonal one (each kept
+    coefficient moves by at most q/2, so SSE differs by <= n_kept q^2 / 4 + 2 sqrt(SSE n_kept) q / 2);
+    huge step (q > 2 max|Z|): every k = 0, x^ = 0, SSE = sum x^2 for every r."""
+    imgs = S.corpus_c2(2, 32, 32)
+    nblk = imgs.shape[0] * 16
+    for r in (1, 6, 21, 50):
+        q = 1.0 / 1024
+        sz = O.compress_zonal_sse(imgs, r)
+        sq = O.compress_quant_sse(imgs, q, r)
+        nk = r * nblk / imgs.shape[0]
+        assert np.all(np.abs(sq - sz) <= nk * q * q / 4 + q * np.sqrt(sz * nk) + 1e-9), r
+        big = O.compress_quant_sse(imgs, 8192.0, r)
+        assert np.allclose(big, (imgs.astype(np.float64) ** 2).sum(axis=(1, 2)), rtol=1e-12)
+
+
 def test_P18_quant_constant_image_closed_form():
     for v in range(256):
         img = np.full((8, 16), v, dtype=np.uint8)
@@ -330,6 +406,24 @@ def test_P18_quant_constant_image_closed_form():
         assert np.abs(rec - want).max() < 1e-9
         sse = O.compress_quant_sse(img, 16.0)[0]
         assert abs(sse - (0 if v % 2 == 0 else 128)) < 1e-7
+        # a constant block has only the DC coefficient, which every r >= 1 keeps (R17)
+        assert abs(O.compress_quant_sse(img, 16.0, 1)[0] - sse) < 1e-7
+
+
+def test_inverse_from_coefficients_and_exact_u8_rounding():
+    """reconstruct_from_coef_exact on a forward's output equals the pinned zonal twin (P8 / P15), its
+    r = 64 inverse of any plane equals 576 x the float64 literal inverse C^T (D Y D) C, and
+    round_u8_exact576 equals round_u8 of R / 576 away from exact ties and rounds ties away from 0."""
+    imgs = np.concatenate([S.corpus_c2(2, 16, 24), rng.integers(0, 256, (2, 16, 24), dtype=np.uint8)])
+    for r in (1, 10, 36, 64):
+        assert np.array_equal(O.reconstruct_from_coef_exact(O.forward_int(imgs), r), O.reconstruct_zonal_exact(imgs, r))
+    Y = rng.integers(-32768, 32768, (3, 16, 24))
+    d = np.array([8, 6, 4, 6, 8, 6, 4, 6], dtype=float)
+    Z = O.from_blocks(O.to_blocks(Y) / np.sqrt(np.outer(d, d)))
+    R = O.reconstruct_from_coef_exact(Y, 64)
+    assert np.allclose(R / 576.0, O.inverse(Z), rtol=1e-12, atol=1e-6)
+    R = np.array([-1000, -289, -288, -1, 0, 287, 288, 289, 863, 864, 146591, 146592, 10 ** 7])
+    assert O.round_u8_exact576(R).tolist() == [0, 0, 0, 0, 0, 0, 1, 1, 1, 2, 254, 255, 255]
 
 
 def test_u8_rounding():

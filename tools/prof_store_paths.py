@@ -1,5 +1,5 @@
 """Driver for an ncu capture of the TMA bulk-store paths: the C3 forward (8192 x 512^2 -> int16,
-k_forward_tma<I16>), the standalone inverse int16 -> f32 / u8 (k_inverse_i16_tma) and the zonal
+k_forward_tma<I16>), the standalone inverse int16 -> f32 / u8 (k_inverse_tma<IN, RECON>) and the zonal
 compress with an f32 / u8 reconstruction (k_compress_recon), 16 x 4096^2 C5-kind images."""
 import os
 import sys
