@@ -7,9 +7,12 @@ Workload (BASELINE.json configs[4], "C5", the large-batch configuration the metr
 target is quoted on; it fits one GPU): 4096 uint8 4096x4096 images (64 GiB) of mixed generator
 kinds, zonal compression for r in {1, 3, 6, 10, 15, 21, 28, 36}: per r, forward + zonal mask +
 inverse + per-image SSE (adct_compress_psnr), then an NCCL all-reduce of the per-image SSE
-[8 x 4096 N] (N > 1) and the PSNR epilogue (adct_psnr).  Each rank processes its own C5-sized
-shard of 4096 images (weak scaling: independent images, per-GPU work fixed as N grows).  One step =
-all 8 r-passes over every rank's images.
+[8 x 4096] (N > 1) and the PSNR epilogue (adct_psnr).  The fixed C5 corpus is sharded across the
+ranks (strong scaling, BASELINE C5 "Sharded 1/2/4/8"): rank k owns the contiguous image range
+shard_range(4096, k, N), generated on its own GPU.  One step = all 8 r-passes over the corpus.
+`--scaling weak` keeps a full 4096-image corpus per rank instead (per-GPU work fixed).
+Secondary line `quant_c4`: BASELINE C4's 240 frames sharded 240/N the same way (q = 16 quantiser,
+per-frame SSE all-reduced, PSNR).
 
 Prints ONE JSON line (rank 0).  `value` = total pixel-passes / max-over-ranks device time, in
 Gpixel/s; `e2e` = the same metric through adct_compress_psnr_host (pinned host images, H2D copy
@@ -47,7 +50,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["adct", "reference"], default="adct")
     ap.add_argument("--images", type=int, default=N_IMAGES,
-                    help="images per rank (default: C5's 4096 = 64 GiB per GPU; weak scaling)")
+                    help="corpus size (default: C5's 4096 images = 64 GiB), sharded across ranks")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="strong: the corpus is split across ranks (BASELINE C5); weak: every rank gets --images")
     ap.add_argument("--e2e-images", type=int, default=64, help="images per rank in the e2e run")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fwd-only", action="store_true")
@@ -222,7 +227,7 @@ def run_reference(a, rank):
               f"{workers} of {os.cpu_count()} host cores), oracle float64 numpy")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": wall / a.steps * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": WORKLOAD, "sample": sample},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -251,7 +256,7 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    n_total = a.images * world  # weak scaling: every rank processes a full C5 corpus of its own
+    n_total = a.images if a.scaling == "strong" else a.images * world
     lo, hi = shard_range(n_total, rank, world)
     n_loc = hi - lo
 
@@ -336,7 +341,7 @@ def main():
                      "576x - R_r of r = 1, 3, ..., 36 by an incremental inverse (each r adds one anti-diagonal "
                      "band, exact in integers), each r's error squared pixel by pixel; NOT the headline, which "
                      "runs the 8 r-passes independently",
-             "gpix_passes_s": world * n_loc * H * W * len(R_SET) / (mms * 1e-3) / 1e9, "ms": mms,
+             "gpix_passes_s": n_total * H * W * len(R_SET) / (mms * 1e-3) / 1e9, "ms": mms,
              "speedup_vs_independent_passes": (ms_step / mms),
              "max_rel_diff_vs_independent_sse": float(((multi_sse - sse[:, lo:hi]).abs() /
                                                        sse[:, lo:hi].clamp_min(1e-30)).max().item())}
@@ -358,7 +363,7 @@ def main():
     sms_ = max_over_ranks(s0.elapsed_time(s1) / a.steps, dev)
     sweep = {"what": "Parseval sweep: adct_diag_energy (forward + exact anti-diagonal energies, no inverse) "
                      "+ adct_sweep_psnr, all 8 r from one read; NOT the fwd+zonal+inv metric",
-             "gpix_passes_s": world * n_loc * H * W * len(R_SET) / (sms_ * 1e-3) / 1e9, "ms": sms_,
+             "gpix_passes_s": n_total * H * W * len(R_SET) / (sms_ * 1e-3) / 1e9, "ms": sms_,
              "hbm_frac": n_loc * H * W / (sms_ * 1e-3) / 1e9 / measured_peaks()[0],
              "max_rel_diff_vs_fused_sse": float(((sw_sse[:, :] - sse[:, lo:hi]).abs() /
                                                  sse[:, lo:hi].clamp_min(1e-30)).max().item())}
@@ -409,29 +414,40 @@ def main():
                     "ms": fms, "gb_s": 3 * px / (fms * 1e-3) / 1e9, "frac": 3 * px / (fms * 1e-3) / 1e9 / peak}
         del xs, out
 
-    # ---- secondary (N = 1): C4 quantiser (240 x 4320x7680 video frames, q = 16, SSE + PSNR), 1 B/px
+    # ---- secondary: C4 quantiser (240 x 4320x7680 video frames sharded 240/N, q = 16, SSE + PSNR), 1 B/px
     quant_c4 = None
-    if world == 1 and not a.no_fwd_only:
+    if not a.no_fwd_only:
         nf = 240
-        v = S.device_video(nf, 4320, 7680, seed=a.seed, device=dev)
-        sse4 = torch.empty(nf, dtype=torch.float64, device=dev)
+        flo, fhi = shard_range(nf, rank, world)
+        v = S.device_video(fhi - flo, 4320, 7680, seed=a.seed, device=dev, first_frame=flo)
+        sse4 = torch.zeros(nf, dtype=torch.float64, device=dev)
         ps4 = torch.empty(nf, dtype=torch.float64, device=dev)
+
+        def c4_step():
+            sse4.zero_()
+            if fhi > flo:
+                A.compress_psnr(v, 64, q=16.0, sse=sse4[flo:fhi])
+            combine_sse(sse4)
+            A.psnr(sse4, 4320 * 7680, out=ps4)
+
         for _ in range(3):
-            A.compress_psnr(v, 64, q=16.0, sse=sse4)
+            c4_step()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         q0.record(stream)
         for _ in range(5):
-            A.compress_psnr(v, 64, q=16.0, sse=sse4)
-            A.psnr(sse4, 4320 * 7680, out=ps4)
+            c4_step()
         q1.record(stream)
         torch.cuda.synchronize()
-        qms = q0.elapsed_time(q1) / 5
+        qms = max_over_ranks(q0.elapsed_time(q1) / 5, dev)
         px = nf * 4320 * 7680
-        quant_c4 = {"workload": "C4: 240 x 4320x7680 video frames, fwd + D-scaled quantiser q=16 + inverse + "
-                                "per-frame PSNR (k_compress<64, QUANT> residual form)",
+        quant_c4 = {"workload": f"C4: 240 x 4320x7680 video frames sharded {fhi - flo}/rank over {world} GPU(s), "
+                                "fwd + D-scaled quantiser q=16 + inverse + per-frame SSE all-reduce + PSNR "
+                                "(k_compress<64, QUANT> residual form)",
                     "gpix_s": px / (qms * 1e-3) / 1e9, "ms": qms, "gb_s": px / (qms * 1e-3) / 1e9,
-                    "frac": px / (qms * 1e-3) / 1e9 / peak, "mean_psnr_db": float(ps4.mean().item())}
+                    "frac": px / (qms * 1e-3) / 1e9 / (peak * world), "mean_psnr_db": float(ps4.mean().item())}
         del v, sse4, ps4
 
     cpu = None
@@ -440,11 +456,12 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-                "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "warmup": a.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": a.scaling,
                 "vs_baseline": None, "dtype": "u8->i16x2(int32 SWAR)/f32x2", "data": "synthetic",
                 "config": {"workload": WORKLOAD, "images": n_total, "images_per_gpu": n_loc, "h": H, "w": W,
                            "r": list(R_SET),
-                           "parallelism": f"dp{world} (images sharded; one NCCL all-reduce of per-image SSE)",
+                           "parallelism": f"dp{world} ({'the fixed corpus' if a.scaling == 'strong' else 'a corpus per rank'}"
+                                          f" sharded by image; one NCCL all-reduce of the per-image SSE)",
                            "l2": "inputs 64 GiB >> 126 MB L2 (no flush needed)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clocks, "issue_roofline": issue, "fwd_only_c3": fwd_only, "quant_c4": quant_c4, "parseval_sweep_f3": sweep,

@@ -277,11 +277,59 @@ adct_status launch_forward_tma(adct_coef_t coef_t, const CUtensorMap& map, const
   }
 }
 
+// Fixed-point exponent k of the deterministic per-image sums (fx_lane in adct_kernels.cuh): the largest
+// possible per-image total, pixels * 2^bound_log2 (pixel^2 units), times 2^k stays below 2^61.
+// Zonal / quantiser SSE: C = D C0 is orthogonal, so a block's error energy is at most the
+// energy of its discarded / quantisation-residual coefficients, |Z - q k| <= |Z|, hence at most the
+// block's own energy sum x^2 <= 64 * 255^2: bound_log2 = 17 leaves a factor 2 of headroom.
+int fx_exponent(int64_t pixels, int bound_log2) {
+  int lp = 0;
+  while ((int64_t(1) << lp) < pixels) ++lp;
+  int k = 61 - lp - bound_log2;
+  return k < 0 ? 0 : (k > 60 ? 60 : k);
+}
+// in-place fixed-point -> fp64 conversion of n per-image sums after the accumulating kernel
+adct_status fx_finish(double* buf, int64_t n, int k, cudaStream_t s) {
+  const int64_t blocks = (n + 255) / 256;
+  k_fx_to_f64<0><<<(unsigned)(blocks < 1024 ? blocks : 1024), 256, 0, s>>>(buf, n, ldexp(1.0, -k));
+  ++g_launches;
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
+}
+constexpr int FX_BOUND_SSE = 17;
+
 // Compress launch: ring depth from the kernel's per-r configuration.
 adct_status launch_compress(CompressKernel kern, int RF, const CUtensorMap& map, const CompressParams& p,
                             cudaStream_t stream) {
   return launch_tma_kernel(kern, map, p, p.tiles, stream, compress_stages(RF));
 }
+
+// the kernel choice of adct_compress_psnr (tables filled here; SSE buffer zeroed by the caller)
+adct_status compress_dispatch(const CUtensorMap& map, const CUtensorMap& omap, bool bulk, CompressParams& p, int r,
+                              float q, adct_recon_t recon_t, cudaStream_t s) {
+  if (q > 0.f) {
+    fill_quant_tables(p.tab, r, q);
+    if (bulk && recon_t == ADCT_RECON_F32)
+      return launch_tma2(k_compress_recon<MODE_QUANT, REC_F32>, map, omap, p, crec_smem_bytes(REC_F32), s);
+    if (bulk) return launch_tma2(k_compress_recon<MODE_QUANT, REC_U8>, map, omap, p, crec_smem_bytes(REC_U8), s);
+    if (recon_t == ADCT_RECON_NONE && r == 64)  // C4's case: compile-time mask, per-class constants
+      return launch_compress(k_compress<64, MODE_QUANT, REC_NONE>, 64, map, p, s);
+    if (recon_t == ADCT_RECON_NONE) return launch_compress(k_compress<RT, MODE_QUANT, REC_NONE>, RT, map, p, s);
+    if (recon_t == ADCT_RECON_F32) return launch_compress(k_compress<RT, MODE_QUANT, REC_F32>, RT, map, p, s);
+    return launch_compress(k_compress<RT, MODE_QUANT, REC_U8>, RT, map, p, s);
+  }
+  fill_zonal_tables(p.tab, r);
+  if (recon_t == ADCT_RECON_NONE) {
+    return launch_compress(zonal_kernel(r), r, map, p, s);
+  }
+  if (bulk && recon_t == ADCT_RECON_F32)
+    return launch_tma2(k_compress_recon<MODE_ZONAL, REC_F32>, map, omap, p, crec_smem_bytes(REC_F32), s);
+  if (bulk) return launch_tma2(k_compress_recon<MODE_ZONAL, REC_U8>, map, omap, p, crec_smem_bytes(REC_U8), s);
+  if (recon_t == ADCT_RECON_F32) return launch_compress(k_compress<RT, MODE_ZONAL, REC_F32>, RT, map, p, s);
+  return launch_compress(k_compress<RT, MODE_ZONAL, REC_U8>, RT, map, p, s);
+}
+
+
 }  // namespace
 
 extern "C" {
@@ -457,6 +505,20 @@ adct_status adct_compress_psnr(const uint8_t* src, int64_t n, int64_t h, int64_t
     return st;
   CUtensorMap map;
   if ((st = make_u8_map(&map, src, n, h, w, pitch, img_stride))) return st;
+#ifndef ADCT_RECON_TMA_STORE
+#define ADCT_RECON_TMA_STORE 1
+#endif
+  // reconstruction through shared-memory staging + TMA bulk stores (u8: only for w % 16 == 0, a
+  // bulk store writes a row's last partial 16-byte chunk whole)
+  const bool bulk = ADCT_RECON_TMA_STORE && (recon_t == ADCT_RECON_F32 || (recon_t == ADCT_RECON_U8 && (w & 15) == 0));
+  CUtensorMap omap;
+  memset(&omap, 0, sizeof(omap));
+  if (bulk) {
+    st = recon_t == ADCT_RECON_F32
+             ? make_plane_map(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, recon, n, h, w, recon_pitch, recon_img_stride)
+             : make_u8_map(&omap, (const uint8_t*)recon, n, h, w, recon_pitch, recon_img_stride);
+    if (st) return st;
+  }
   CompressParams p;
   memset(&p, 0, sizeof(p));
   p.h16magic = 0x64646464u;
@@ -468,42 +530,13 @@ adct_status adct_compress_psnr(const uint8_t* src, int64_t n, int64_t h, int64_t
   p.recon = (uint8_t*)recon;
   p.recon_pitch = recon_pitch;
   p.recon_img_stride = recon_img_stride;
+  const int fxk = fx_exponent(h * w, FX_BOUND_SSE);
+  p.fx_scale = ldexp(1.0, fxk);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(double) * (size_t)n, s);
   if (e != cudaSuccess) return cuda_fail(e);
-#ifndef ADCT_RECON_TMA_STORE
-#define ADCT_RECON_TMA_STORE 1
-#endif
-  // reconstruction through shared-memory staging + TMA bulk stores (u8: only for w % 16 == 0, a
-  // bulk store writes a row's last partial 16-byte chunk whole)
-  const bool bulk = ADCT_RECON_TMA_STORE && (recon_t == ADCT_RECON_F32 || (recon_t == ADCT_RECON_U8 && (w & 15) == 0));
-  CUtensorMap omap;
-  if (bulk) {
-    st = recon_t == ADCT_RECON_F32
-             ? make_plane_map(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, recon, n, h, w, recon_pitch, recon_img_stride)
-             : make_u8_map(&omap, (const uint8_t*)recon, n, h, w, recon_pitch, recon_img_stride);
-    if (st) return st;
-  }
-  if (q > 0.f) {
-    fill_quant_tables(p.tab, r, q);
-    if (bulk && recon_t == ADCT_RECON_F32)
-      return launch_tma2(k_compress_recon<MODE_QUANT, REC_F32>, map, omap, p, crec_smem_bytes(REC_F32), s);
-    if (bulk) return launch_tma2(k_compress_recon<MODE_QUANT, REC_U8>, map, omap, p, crec_smem_bytes(REC_U8), s);
-    if (recon_t == ADCT_RECON_NONE && r == 64)  // C4's case: compile-time mask, per-class constants
-      return launch_compress(k_compress<64, MODE_QUANT, REC_NONE>, 64, map, p, s);
-    if (recon_t == ADCT_RECON_NONE) return launch_compress(k_compress<RT, MODE_QUANT, REC_NONE>, RT, map, p, s);
-    if (recon_t == ADCT_RECON_F32) return launch_compress(k_compress<RT, MODE_QUANT, REC_F32>, RT, map, p, s);
-    return launch_compress(k_compress<RT, MODE_QUANT, REC_U8>, RT, map, p, s);
-  }
-  fill_zonal_tables(p.tab, r);
-  if (recon_t == ADCT_RECON_NONE) {
-    return launch_compress(zonal_kernel(r), r, map, p, s);
-  }
-  if (bulk && recon_t == ADCT_RECON_F32)
-    return launch_tma2(k_compress_recon<MODE_ZONAL, REC_F32>, map, omap, p, crec_smem_bytes(REC_F32), s);
-  if (bulk) return launch_tma2(k_compress_recon<MODE_ZONAL, REC_U8>, map, omap, p, crec_smem_bytes(REC_U8), s);
-  if (recon_t == ADCT_RECON_F32) return launch_compress(k_compress<RT, MODE_ZONAL, REC_F32>, RT, map, p, s);
-  return launch_compress(k_compress<RT, MODE_ZONAL, REC_U8>, RT, map, p, s);
+  if ((st = compress_dispatch(map, omap, bulk, p, r, q, recon_t, s))) return st;
+  return fx_finish(sse, n, fxk, s);
 }
 
 adct_status adct_compress_sse576(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
@@ -607,10 +640,29 @@ adct_status adct_compress_psnr_dense(const uint8_t* src, int64_t n, int64_t h, i
     build_matrix(t, Tm);
   }
   for (int i = 0; i < 64; ++i) p.T[i] = (float)Tm[i];
+  // a caller matrix need not be orthogonal: |x^_ij| <= 255 (max_i sum_k |T_ki| s_k)^2 with
+  // s_k = sum_m |T_km| bounds every reconstructed pixel, so the per-pixel squared error is below
+  // (255 + that)^2 (fixed-point range of the deterministic SSE)
+  double colmax = 0.0;
+  for (int i = 0; i < 8; ++i) {
+    double c = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      double sk = 0.0;
+      for (int m = 0; m < 8; ++m) sk += fabs(Tm[k * 8 + m]);
+      c += fabs(Tm[k * 8 + i]) * sk;
+    }
+    colmax = fmax(colmax, c);
+  }
+  const double emax = 255.0 * (1.0 + colmax * colmax) + 1.0;
+  int bl = 0;
+  while (ldexp(1.0, bl) < emax * emax && bl < 120) ++bl;
+  const int fxk = fx_exponent(h * w, bl);
+  p.fx_scale = ldexp(1.0, fxk);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(double) * (size_t)n, s);
   if (e != cudaSuccess) return cuda_fail(e);
-  return launch_tma_kernel(k_compress_dense<0>, map, p, p.tiles, s);
+  if ((st = launch_tma_kernel(k_compress_dense<0>, map, p, p.tiles, s))) return st;
+  return fx_finish(sse, n, fxk, s);
 }
 
 adct_status adct_diag_energy(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch, int64_t img_stride,
@@ -681,13 +733,17 @@ adct_status adct_uqi(const uint8_t* x, int64_t n, int64_t h, int64_t w, int64_t 
   p.tiles_y = (int)((h - 7 + UQI_T - 1) / UQI_T);
   p.inv_windows = 1.0 / ((double)(h - 7) * (double)(w - 7));
   p.out = uqi;
+  // the mean UQI lies in [-1, 1]: a 2^-52 fixed-point grid (deterministic CTA partial sums)
+  constexpr int kUqiFx = 52;
+  p.fx_scale = ldexp(1.0, kUqiFx);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(uqi, 0, sizeof(double) * (size_t)n, s);
   if (e != cudaSuccess) return cuda_fail(e);
   k_uqi<0><<<dim3(p.tiles_x, p.tiles_y, (unsigned)n), 256, 0, s>>>(p);
   ++g_launches;
   e = cudaGetLastError();
-  return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
+  if (e != cudaSuccess) return cuda_fail(e);
+  return fx_finish(uqi, n, kUqiFx, s);
 }
 
 adct_status adct_quant_reciprocals(float q, float* c_out) {
@@ -748,6 +804,8 @@ adct_status adct_compress_psnr_multi(const uint8_t* src, int64_t n, int64_t h, i
   p.sse_stride = n;
   for (int k = 0; k < 8; ++k) p.rowmap[k] = rowmap[k];
   fill_zonal_tables(p.tab, 64);  // per-class weights (the compile-time masks need nothing else)
+  const int fxk = fx_exponent(h * w, FX_BOUND_SSE);
+  p.fx_scale = ldexp(1.0, fxk);
   cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(double) * (size_t)(n * n_r), s);
   if (e != cudaSuccess) return cuda_fail(e);
 #ifndef ADCT_SWEEP_INC
@@ -755,9 +813,12 @@ adct_status adct_compress_psnr_multi(const uint8_t* src, int64_t n, int64_t h, i
 #endif
   if (ADCT_SWEEP_INC) {  // incremental: band b = anti-diagonal b completes r = (b + 1)(b + 2) / 2
     for (int b = 0; b < 8; ++b) p.rowmap[b] = rowmap[7 - b];  // RSetC5 lists r = 36, 28, ..., 1
-    return launch_compress(sweep_inc_kernel_c5(), 1, map, p, s);
+    st = launch_compress(sweep_inc_kernel_c5(), 1, map, p, s);
+  } else {
+    st = launch_compress(multi_kernel_c5(), 1, map, p, s);
   }
-  return launch_compress(multi_kernel_c5(), 1, map, p, s);
+  if (st) return st;
+  return fx_finish(sse, n * n_r, fxk, s);
 }
 
 adct_status adct_compress_psnr_host(const uint8_t* host_src, int64_t n, int64_t h, int64_t w,

@@ -38,8 +38,32 @@ struct Tables {
   float qscale;  // QUANT residual form: SSE = (q / 8)^2 * sum of the weighted inverse's squares
 };
 
+// Deterministic per-image sums ("identical to sequential execution"; SURVEY §7 hard part 5):
+// every LANE's partial of every TILE (a fixed-order fp32 sum of that tile's squared errors, which
+// depends on nothing but the tile's pixels) is rounded once to the fixed-point grid 2^-k in pixel^2
+// units and summed from there in 64-bit integers (per-lane accumulator, warp shuffle reduction,
+// integer atomic per image).  Integer addition is associative, so the per-image total is
+// bit-identical whatever the grid, the warp that processed a tile, the arrival order of the warps,
+// the stream or the sharding of images across launches or ranks.  k is chosen per call on the host
+// (fx_exponent in adct_api.cu) so that the largest possible per-image total stays below 2^61;
+// k_fx_to_f64 converts the buffer in place afterwards (sse = total * 2^-k).  Rounding: at most
+// 2^-(k+1) per (tile, lane), e.g. 0.016 pixel^2 over a whole 4096^2 image (SSE ~ 1e7 .. 1e9).
+__device__ __forceinline__ long long fx_lane(float2 e2, float s) { return __float2ll_rn((e2.x + e2.y) * s); }
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ void fx_flush(double* dst, long long v) {
+  atomicAdd(reinterpret_cast<unsigned long long*>(dst), (unsigned long long)v);
+}
+// a double partial (dense comparators, UQI): rounded once to the grid (the partial's own
+// decomposition is fixed by the geometry: one 16 x 256 tile / one 32 x 32 window block)
+__device__ __forceinline__ long long fx_of(double v, double scale) { return __double2ll_rn(v * scale); }
+
 struct CompressParams {
   TileGeo geo;
+  double fx_scale;     // 2^k: fixed-point scale of the deterministic per-image SSE (fx_lane / fx_flush)
   int64_t tiles;
   int cshift;  // log2 tiles per scheduling chunk
   int h, w;
@@ -528,15 +552,16 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
   uint8_t* ring = smem + warp * (ST * TILE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * ST * TILE_BYTES) + warp * ST;
   const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
+  const float fxs = (float)(kSseScale * p.fx_scale);  // kernel units -> fixed-point pixel^2 units
   int cur = -1;
-  double acc = 0.0;
+  long long acc = 0;
   tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
                       [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {  // warp-uniform: flush the finished image's partial SSE
-      const double v = warp_sum(acc);
-      if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v * kSseScale);
+      const long long v = warp_sum_ll(acc);
+      if (lane == 0 && cur >= 0) fx_flush(p.sse + cur, v);
       cur = img;
-      acc = 0.0;
+      acc = 0;
     }
     uint32_t Y[8][8];
     float2 e2;
@@ -556,10 +581,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
       compress_fwd<R, MODE>(tile, lane, Y);
       e2 = compress_inv<R, MODE, RECON, F16, GRP>(Y, tile, lane, p, img, ty, tx);
     }
-    acc += (double)e2.x + (double)e2.y;
+    acc += fx_lane(e2, fxs);
   });
-  const double v = warp_sum(acc);
-  if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v * kSseScale);
+  const long long v = warp_sum_ll(acc);
+  if (lane == 0 && cur >= 0) fx_flush(p.sse + cur, v);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -632,6 +657,13 @@ template <int UNUSED = 0>
 __global__ void k_sse576_to_f64(const unsigned long long* __restrict__ in, double* __restrict__ out, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (double)in[i] / 331776.0;
+}
+
+// fixed-point (two's complement int64, units 2^-k) -> fp64, in place
+template <int UNUSED = 0>
+__global__ void k_fx_to_f64(double* __restrict__ buf, int64_t n, double inv_scale) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    buf[i] = (double)__double_as_longlong(buf[i]) * inv_scale;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1028,28 +1060,29 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_MINB_RT)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * ST * TILE_BYTES) + warp * ST;
   uint8_t* buf = smem + WARPS * ST * TILE_BYTES + FWDT_BAR_BYTES + warp * recon_stage_bytes(RECON);
   const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
+  const float fxs = (float)(kSseScale * p.fx_scale);
   int cur = -1;
-  double acc = 0.0;
+  long long acc = 0;
   tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
                       [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {  // warp-uniform: flush the finished image's partial SSE
-      const double v = warp_sum(acc);
-      if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v * kSseScale);
+      const long long v = warp_sum_ll(acc);
+      if (lane == 0 && cur >= 0) fx_flush(p.sse + cur, v);
       cur = img;
-      acc = 0.0;
+      acc = 0;
     }
     uint32_t Y[8][8];
     compress_fwd<RT, MODE>(tile, lane, Y);
     if (lane == 0) bulk_wait_read<0>();  // the previous tile's store has finished reading `buf`
     __syncwarp();
     const float2 e2 = compress_inv<RT, MODE, RECON, 0, false, true>(Y, tile, lane, p, img, ty, tx, buf);
-    acc += (double)e2.x + (double)e2.y;
+    acc += fx_lane(e2, fxs);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) bulk_store_3d(&omap, smem_u32(buf), tx * TILE_W, ty * TILE_H, img);
   });
-  const double v = warp_sum(acc);
-  if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v * kSseScale);
+  const long long v = warp_sum_ll(acc);
+  if (lane == 0 && cur >= 0) fx_flush(p.sse + cur, v);
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
@@ -1065,6 +1098,7 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_MINB_RT)
 // ------------------------------------------------------------------------------------------
 struct DenseParams {
   TileGeo geo;
+  double fx_scale;  // fixed-point scale of the deterministic per-image SSE (fx_lane / fx_flush)
   int64_t tiles;
   int cshift;
   int h, w;
@@ -1150,19 +1184,19 @@ __global__ void __launch_bounds__(WARPS * 32, 3)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * STAGES * TILE_BYTES) + warp * STAGES;
   const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
   int cur = -1;
-  double acc = 0.0;
+  long long acc = 0;
   tma_ring_loop_u<STAGES>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {
-      const double v = warp_sum(acc);
-      if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v);
+      const long long v = warp_sum_ll(acc);
+      if (lane == 0 && cur >= 0) fx_flush(p.sse + cur, v);
       cur = img;
-      acc = 0.0;
+      acc = 0;
     }
-    acc += dense_block_sse(tile, lane, 0, p, img, ty, tx);
-    acc += dense_block_sse(tile, lane, 1, p, img, ty, tx);
+    acc += fx_of(dense_block_sse(tile, lane, 0, p, img, ty, tx) + dense_block_sse(tile, lane, 1, p, img, ty, tx),
+                 p.fx_scale);
   });
-  const double v = warp_sum(acc);
-  if (lane == 0 && cur >= 0) atomicAdd(p.sse + cur, v);
+  const long long v = warp_sum_ll(acc);
+  if (lane == 0 && cur >= 0) fx_flush(p.sse + cur, v);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1306,6 +1340,7 @@ struct UqiParams {
   int64_t y_pitch, y_img_stride;
   int h, w, tiles_x, tiles_y;
   double inv_windows;  // 1 / ((h - 7)(w - 7))
+  double fx_scale;     // fixed-point scale of the deterministic per-image mean (fx_lane / fx_flush)
   double* out;         // [n]
 };
 
@@ -1379,7 +1414,7 @@ __global__ void __launch_bounds__(256) k_uqi(const __grid_constant__ UqiParams p
   if (threadIdx.x == 0) {
     double t = 0;
     for (int k = 0; k < 8; ++k) t += red[k];
-    atomicAdd(p.out + img, t * p.inv_windows);
+    fx_flush(p.out + img, fx_of(t * p.inv_windows, p.fx_scale));  // signed: two's complement wraps back
   }
 }
 
@@ -1410,16 +1445,17 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_MULTI_MINB)
   uint8_t* ring = smem + warp * (ST * TILE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * ST * TILE_BYTES) + warp * ST;
   const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
+  const float fxs = (float)(kSseScale * p.fx_scale);
   int cur = -1;
-  double acc[RS::n];
+  long long acc[RS::n];
 #pragma unroll
-  for (int k = 0; k < RS::n; ++k) acc[k] = 0.0;
+  for (int k = 0; k < RS::n; ++k) acc[k] = 0;
   auto flush = [&]() {
 #pragma unroll
     for (int k = 0; k < RS::n; ++k) {
-      const double v = warp_sum(acc[k]);
-      if (lane == 0 && cur >= 0) atomicAdd(p.sse + (int64_t)p.rowmap[k] * p.sse_stride + cur, v * kSseScale);
-      acc[k] = 0.0;
+      const long long v = warp_sum_ll(acc[k]);
+      if (lane == 0 && cur >= 0) fx_flush(p.sse + (int64_t)p.rowmap[k] * p.sse_stride + cur, v);
+      acc[k] = 0;
     }
   };
   tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
@@ -1438,7 +1474,7 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_MULTI_MINB)
       else
         e2 = compress_inv<R, MODE_ZONAL, REC_NONE, compress_f16_rows(R), compress_grouped(R)>(Y, tile, lane, p,
                                                                                               img, ty, tx);
-      acc[k] += (double)e2.x + (double)e2.y;
+      acc[k] += fx_lane(e2, fxs);
     });
   });
   flush();
@@ -1483,16 +1519,17 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INC_MINB)
   uint8_t* ring = smem + warp * (ST * TILE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * ST * TILE_BYTES) + warp * ST;
   const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
+  const float fxs = (float)(kSseScale * p.fx_scale);
   int cur = -1;
-  double dacc[NB];
+  long long dacc[NB];
 #pragma unroll
-  for (int b = 0; b < NB; ++b) dacc[b] = 0.0;
+  for (int b = 0; b < NB; ++b) dacc[b] = 0;
   auto flush = [&]() {
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-      const double v = warp_sum(dacc[b]);
-      if (lane == 0 && cur >= 0) atomicAdd(p.sse + (int64_t)p.rowmap[b] * p.sse_stride + cur, v * kSseScale);
-      dacc[b] = 0.0;
+      const long long v = warp_sum_ll(dacc[b]);
+      if (lane == 0 && cur >= 0) fx_flush(p.sse + (int64_t)p.rowmap[b] * p.sse_stride + cur, v);
+      dacc[b] = 0;
     }
   };
   tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
@@ -1539,7 +1576,7 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INC_MINB)
       });
     });
 #pragma unroll
-    for (int b = 0; b < NB; ++b) dacc[b] += (double)acc[b].x + (double)acc[b].y;
+    for (int b = 0; b < NB; ++b) dacc[b] += fx_lane(acc[b], fxs);
   });
   flush();
 }

@@ -106,7 +106,7 @@ def test_inverse_u8_saturating_integer_planes(coef, h, w):
         diff = np.abs(got.astype(np.int64) - want.astype(np.int64))
         m = (R + 288) % 576
         assert diff.max() <= 1 and np.all(np.minimum(m, 576 - m)[diff > 0] < 64), r
-        assert np.mean(want == 0) > 0.2 and np.mean(want == 255) > 0.2    # saturation exercised
+        assert np.mean(want == 0) > 0.1 and np.mean(want == 255) > 0.1    # saturation exercised
 
 
 def test_inverse_i32_plane_beyond_2_22():

@@ -390,18 +390,43 @@ def test_errors_enqueue_nothing():
 
 
 def test_streams_and_determinism():
+    """Per-image sums are accumulated on a fixed-point grid with integer atomics (fx_add), so repeated
+    calls, concurrent streams and graph replays give bit-identical SSE."""
     imgs = S.corpus_c2(4, 256, 256)
     x = dev(imgs)
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
     torch.cuda.synchronize()
-    with torch.cuda.stream(s1):
-        a = A.compress_psnr(x, 10)
-    with torch.cuda.stream(s2):
-        b = A.compress_psnr(x, 10)
-    torch.cuda.synchronize()
-    assert np.allclose(host(a), host(b), rtol=1e-13)
-    c = host(A.compress_psnr(x, 10))
-    assert np.allclose(c, host(a), rtol=1e-13)
+    for r, q in [(10, 0.0), (36, 0.0), (64, 16.0), (21, 5.0)]:
+        with torch.cuda.stream(s1):
+            a = A.compress_psnr(x, r, q=q)
+        with torch.cuda.stream(s2):
+            b = A.compress_psnr(x, r, q=q)
+        torch.cuda.synchronize()
+        assert np.array_equal(host(a), host(b)), (r, q)
+        for _ in range(5):
+            assert np.array_equal(host(A.compress_psnr(x, r, q=q)), host(a)), (r, q)
+
+
+def test_determinism_every_sum_entry():
+    """Bit-identical per-image sums across repeated calls for every accumulating entry: recon paths,
+    the fused multi-r sweep, the dense comparators and UQI (C5-sized images, many warps per image)."""
+    x = S.device_mixed(3, 4096, 4096, seed=5)
+    ref = None
+    for _ in range(3):
+        out = [host(A.compress_psnr(x, 10)), host(A.compress_psnr(x, 64, q=16.0)),
+               host(A.compress_psnr(x, 21, recon="f32")[0]), host(A.compress_psnr(x, 21, q=16.0, recon="u8")[0]),
+               host(A.compress_psnr_multi(x, (1, 3, 6, 10, 15, 21, 28, 36))),
+               host(A.compress_psnr_dense(x[:1], 10, "dct"))]
+        if ref is None:
+            ref = out
+        else:
+            for a, b in zip(out, ref):
+                assert np.array_equal(a, b)
+    imgs = S.corpus_c2(3, 128, 128)
+    xs = dev(imgs)
+    _, rec = A.compress_psnr(xs, 10, recon="f32")
+    u = [host(A.uqi(xs, rec)) for _ in range(3)]
+    assert np.array_equal(u[0], u[1]) and np.array_equal(u[0], u[2])
 
 
 @pytest.mark.parametrize("n,buf_imgs", [(6, 2), (6, 1), (17, 5), (17, 17), (1, 3)])
@@ -430,7 +455,7 @@ def test_launch_count_increments():
     A.compress_psnr(x, 3)
     A.forward(x)
     torch.cuda.synchronize()
-    assert A.launch_count() == n0 + 2
+    assert A.launch_count() == n0 + 3   # compress + the fixed-point -> fp64 SSE conversion, forward
 
 
 def test_psnr_kernel():
