@@ -60,6 +60,14 @@ def parse():
     return ap.parse_args()
 
 
+def O_psnr(sse, pixels):
+    """PSNR of host SSE values (report-only formatting of device results)."""
+    import numpy as np
+    sse = np.asarray(sse, dtype=np.float64)
+    with np.errstate(divide="ignore"):
+        return np.where(sse == 0, np.inf, 10.0 * np.log10(65025.0 * pixels / np.where(sse == 0, 1, sse)))
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -377,8 +385,10 @@ def main():
     dev_sse = torch.empty((2 * len(R_SET) * ne,), dtype=torch.float64, device=dev)
     host_psnr = torch.empty((len(R_SET), ne), dtype=torch.float64, pin_memory=True)
     del x
+    copy_stream = torch.cuda.Stream()
     for _ in range(max(1, a.warmup)):
-        A.compress_psnr_host(host_imgs, R_SET, dev_buf=dev_buf, dev_sse=dev_sse, host_psnr=host_psnr)
+        A.compress_psnr_host(host_imgs, R_SET, dev_buf=dev_buf, dev_sse=dev_sse, host_psnr=host_psnr,
+                             copy_stream=copy_stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -386,13 +396,14 @@ def main():
     e_steps = max(3, min(a.steps, 10))
     e0.record(stream)
     for _ in range(e_steps):
-        A.compress_psnr_host(host_imgs, R_SET, dev_buf=dev_buf, dev_sse=dev_sse, host_psnr=host_psnr)
+        A.compress_psnr_host(host_imgs, R_SET, dev_buf=dev_buf, dev_sse=dev_sse, host_psnr=host_psnr,
+                             copy_stream=copy_stream)
     e1.record(stream)
     torch.cuda.synchronize()
     ems = max_over_ranks(e0.elapsed_time(e1), dev)
     e2e = {"value": world * ne * H * W * len(R_SET) / (ems / e_steps * 1e-3) / 1e9, "unit": UNIT,
            "h2d_bytes_per_step": ne * H * W, "d2h_bytes_per_step": len(R_SET) * ne * 8,
-           "images_per_rank": ne, "api": "adct_compress_psnr_host"}
+           "images_per_rank": ne, "api": "adct_compress_psnr_host (caller copy stream, fused multi-r kernel)"}
 
     # ---- secondary (N = 1): forward-only C3 (8192 x 512^2 uniform, int16 out), 3 B/px
     fwd_only = None
@@ -450,6 +461,68 @@ def main():
                     "frac": px / (qms * 1e-3) / 1e9 / (peak * world), "mean_psnr_db": float(ps4.mean().item())}
         del v, sse4, ps4
 
+    # ---- secondary (N = 1): C2 sweep (45 x 512^2, r = 1..64: proposed fast path, SDCT integer fast
+    # path, exact DCT dense comparator) and C1 latency (one 512^2 image, r = 10: eager and graph replay)
+    c2_sweep, c1_latency = None, None
+    if world == 1 and not a.no_fwd_only:
+        x2 = A.to_device(S.corpus_c2())
+        s2 = torch.empty((64, 45), dtype=torch.float64, device=dev)
+
+        def r_sweep(fn):
+            for r in range(1, 65):
+                fn(r, s2[r - 1])
+
+        kinds = {"proposed": lambda r, o: A.compress_psnr(x2, r, sse=o),
+                 "sdct_fast": lambda r, o: A.compress_psnr_sdct(x2, r, sse=o),
+                 "dct_dense": lambda r, o: A.compress_psnr_dense(x2, r, "dct", sse=o)}
+        c2_sweep = {"workload": "C2: 45 x 512x512 (seeds 0..44, three kinds), r = 1..64, fwd + zonal + inv + "
+                                "per-image SSE (64 launches per sweep; L2-resident, so no HBM roofline)"}
+        for name, fn in kinds.items():
+            r_sweep(fn)
+            torch.cuda.synchronize()
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            for _ in range(5):
+                r_sweep(fn)
+            c1.record(stream)
+            torch.cuda.synchronize()
+            sms2 = c0.elapsed_time(c1) / 5
+            c2_sweep[name] = {"ms_per_sweep": sms2, "gpix_passes_s": 45 * 512 * 512 * 64 / (sms2 * 1e-3) / 1e9,
+                              "mean_psnr_db_r10": float(np.mean(O_psnr(s2[9].cpu().numpy(), 512 * 512)))}
+        x1 = A.to_device(S.image_c1(0))
+        s1 = torch.empty(1, dtype=torch.float64, device=dev)
+        p1 = torch.empty(1, dtype=torch.float64, device=dev)
+        for _ in range(20):
+            A.compress_psnr(x1, 10, sse=s1)
+            A.psnr(s1, 512 * 512, out=p1)
+        torch.cuda.synchronize()
+        l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0.record(stream)
+        for _ in range(200):
+            A.compress_psnr(x1, 10, sse=s1)
+            A.psnr(s1, 512 * 512, out=p1)
+        l1.record(stream)
+        torch.cuda.synchronize()
+        eager_us = l0.elapsed_time(l1) / 200 * 1e3
+        gs = torch.cuda.Stream()
+        gs.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=gs):
+            A.compress_psnr(x1, 10, sse=s1, stream=gs)
+            A.psnr(s1, 512 * 512, out=p1, stream=gs)
+        for _ in range(20):
+            g.replay()
+        torch.cuda.synchronize()
+        l0.record(stream)
+        for _ in range(200):
+            g.replay()
+        l1.record(stream)
+        torch.cuda.synchronize()
+        c1_latency = {"workload": "C1: one 512x512 image, r = 10, compress + PSNR (3 launches)",
+                      "eager_us_per_call": eager_us, "graph_replay_us_per_call": l0.elapsed_time(l1) / 200 * 1e3,
+                      "psnr_db": float(p1.item())}
+        del x2, s2
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cpu = cpu_oracle_sample(a.seed)
@@ -465,7 +538,7 @@ def main():
                            "l2": "inputs 64 GiB >> 126 MB L2 (no flush needed)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clocks, "issue_roofline": issue, "fwd_only_c3": fwd_only, "quant_c4": quant_c4, "parseval_sweep_f3": sweep,
-                "fused_multi_r_c5": fused,
+                "fused_multi_r_c5": fused, "c2_sweep": c2_sweep, "c1_latency": c1_latency,
                 "mean_psnr_db": {str(r): float(np.mean(ps[k])) for k, r in enumerate(R_SET)}}
         print(json.dumps(line), flush=True)
     if world > 1:

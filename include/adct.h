@@ -83,7 +83,11 @@ adct_status adct_forward(const uint8_t* src, int64_t n, int64_t h, int64_t w, in
 /*
  * adct_inverse — the inverse procedure: X^ = C^T (M_r . Z) C per block.
  * From ADCT_COEF_I16 / I32 (Y) the diagonal is folded as W / 576 (exact integers until the
- * final division); from ADCT_COEF_F32 (Z) the kernel computes T^T (M_r . Z . s) T in fp32.
+ * final division while every node stays below 2^24; int32 values convert exactly to fp32 first);
+ * from ADCT_COEF_F32 (Z) the kernel computes T^T (M_r . Z . s) T in fp32, and values at masked
+ * positions (zig-zag >= r) are ignored even when they are NaN / Inf.  u8 output saturates:
+ * clamp(round_half_away(X^), 0, 255) for any coefficient plane (decided on the integer 576 X^ for
+ * I16 / I32, on the fp32 X^ for F32).
  *   coef  image-shaped coefficient plane (layout as adct_forward's output).
  *   dst   image-shaped reconstruction, dst_t = ADCT_RECON_F32 or ADCT_RECON_U8.
  */
@@ -105,7 +109,14 @@ adct_status adct_inverse(const void* coef, adct_coef_t coef_t, int64_t n, int64_
  *   sse    device double[n], OVERWRITTEN (the call zero-fills it on `stream` first).
  * Quantiser decision: k = round-to-nearest(Y * c) in one fp32 FMA, c the smallest fp32 strictly
  * above 1/(q sqrt(d_i d_j)); equal to the exact round-half-away decision for every reachable Y
- * when q = 16 (exhaustive check: tests/test_quant_decision.py).
+ * when q = 16 (exhaustive check: tests/test_quant_decision.py).  With q > 0 and r < 64 the
+ * coefficients at zig-zag positions >= r are discarded before quantisation (k = 0, reading R17).
+ * Determinism: every per-image sum is accumulated on a fixed-point grid (2^-k pixel^2, k chosen per
+ * call from h * w) from per-tile partials with integer atomics, so sse is bit-identical across
+ * repeated calls, streams, graph replays and any split of the images across calls or ranks.
+ * u8 reconstruction: clamp(round_half_away(X^), 0, 255) for every X^ (saturating; the zonal
+ * decision is taken on the exact integer 576 X^, the quantiser's on the fp32 X^).
+ * Launches: the kernel plus one small fixed-point -> fp64 conversion kernel.
  */
 adct_status adct_compress_psnr(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
                                int64_t img_stride, int r, float q, void* recon,
@@ -149,20 +160,24 @@ adct_status adct_compress_psnr_multi(const uint8_t* src, int64_t n, int64_t h, i
  * adct_compress_psnr_host — end-to-end entry with HOST buffers: copies the images from host
  * memory (pinned recommended; host_src with host_pitch / host_img_stride in bytes) through the
  * caller's device staging buffer `dev_buf` (dev_buf_bytes >= one image of h * w bytes; images are
- * staged compactly, pitch = w rounded up to 16), runs adct_compress_psnr for each of the n_r
- * values r_list[k] (q as above) and adct_psnr, and copies PSNR back to host_psnr[k * n + i].
- *   dev_sse   device double[2 * n_r * n] scratch: SSE in [0, n_r n), PSNR in [n_r n, 2 n_r n).
- *   When dev_buf holds at least two images and n >= 2, the images are staged in chunks of about
- *   n / 8 through two halves of dev_buf on an internal non-blocking copy stream, so the copy of
- *   chunk c+1 overlaps the compress passes of chunk c (event-ordered; the copy stream first waits
- *   for work already queued on `stream`).  Otherwise copy and passes alternate on `stream`.
+ * staged compactly, pitch = w rounded up to 16), compresses them for each of the n_r values
+ * r_list[k] (q as adct_compress_psnr; with q = 0 the set {1, 3, 6, 10, 15, 21, 28, 36} runs as the
+ * fused multi-r kernel of adct_compress_psnr_multi, other sets as independent passes), runs
+ * adct_psnr, and copies PSNR back to host_psnr[k * n + i].
+ *   dev_sse      device double[2 * n_r * n] scratch: SSE in [0, n_r n), PSNR in [n_r n, 2 n_r n).
+ *   copy_stream  optional caller-owned stream (NULL: copies and passes alternate on `stream`).  With
+ *                a copy stream, n >= 2 and dev_buf holding >= two images, the images are staged in
+ *                chunks of about n / 8 through two halves of dev_buf on copy_stream, so the copy of
+ *                chunk c+1 overlaps the passes of chunk c (ordered by events created and released by
+ *                the call; no stream is created; the copy stream first waits for work already queued
+ *                on `stream`).  Every variant is stream-ordered and can be captured into a CUDA graph.
  *   Asynchronous: host_psnr is valid after `stream` is synchronised.
  */
 adct_status adct_compress_psnr_host(const uint8_t* host_src, int64_t n, int64_t h, int64_t w,
                                     int64_t host_pitch, int64_t host_img_stride,
                                     const int* r_list, int n_r, float q, uint8_t* dev_buf,
                                     int64_t dev_buf_bytes, double* dev_sse, double* host_psnr,
-                                    adct_stream_t stream);
+                                    adct_stream_t stream, adct_stream_t copy_stream);
 
 /*
  * Dense comparator / variant path: the same block pipeline with an 8x8
@@ -182,13 +197,31 @@ typedef enum {
   ADCT_T_DCT = 1,
   ADCT_T_SDCT = 2,
   ADCT_T_COARSE = 3,
-  ADCT_T_CUSTOM = 4
+  ADCT_T_CUSTOM = 4,
+  ADCT_T_CEIL = 5 /* F4 ("floor and ceiling functions can be considered instead of the
+                     round-off function"): the orthogonal polar factor (T T^T)^(-1/2) T of
+                     T = ceil(2 C) (entries {0, 1}, det 16; T T^T is not diagonal, so the
+                     orthogonaliser is a dense symmetric matrix and there is no fast algorithm).
+                     floor(2 C) is singular (its DC row floors to 0) and has no entry. */
 } adct_transform_t;
 
 adct_status adct_compress_psnr_dense(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
                                      int64_t img_stride, int r, adct_transform_t t, const double* custom,
                                      float* recon /* nullable f32 plane */, int64_t recon_pitch,
                                      int64_t recon_img_stride, double* sse, adct_stream_t stream);
+
+/*
+ * adct_compress_psnr_sdct — the SDCT comparator (reading R11: sign(C) / (2 sqrt 2)) on the
+ * INTEGER fast path: per block Y = T_s X T_s^T with T_s = sign(C) by the
+ * 24-addition fast algorithm (Table 1) on packed 2 x int16 lanes (exact), the first r
+ * zig-zag coefficients kept, the reconstruction X^ = R / 64 with R = T_s^T (M_r . Y) T_s by the
+ * transposed 24-addition graph (exact integers in fp32), e = 64 x - R exact per pixel, and
+ * sse[i] = per-image sum of (x - X^)^2 (deterministic fixed-point sum, as adct_compress_psnr).
+ * The SDCT is not orthogonal: the transpose is its "approximate inversion".
+ *   src as adct_forward;  sse device double[n], overwritten.
+ */
+adct_status adct_compress_psnr_sdct(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                                    int64_t img_stride, int r, double* sse, adct_stream_t stream);
 
 /*
  * adct_uqi — universal quality index: per image, the mean over all
@@ -218,7 +251,8 @@ adct_status adct_diag_energy(const uint8_t* src, int64_t n, int64_t h, int64_t w
 adct_status adct_sweep_psnr(const uint64_t* energy, int64_t n, int64_t pixels, const int* r_list, int n_r,
                             double* sse, double* psnr, adct_stream_t stream);
 
-/* HOST helper: the library's own 8x8 matrix for t (ADCT_T_PROPOSED..ADCT_T_COARSE), row-major. */
+/* HOST helper: the library's own 8x8 matrix for t (ADCT_T_PROPOSED..ADCT_T_COARSE, ADCT_T_CEIL),
+ * row-major. */
 adct_status adct_transform_matrix(adct_transform_t t, double* out);
 
 /*

@@ -29,6 +29,7 @@ import numpy as np
 __all__ = [
     "dct_matrix", "round_half_away", "c0_matrix", "orthogonalizer", "proposed_matrix",
     "coarse_matrix", "frobenius_optimal_scale", "sdct_matrix", "transfer_error_energy",
+    "roundoff_matrix", "polar_orthogonal", "ceil_matrix", "sdct_sign_matrix",
     "zigzag_order", "zigzag_index", "zonal_mask", "to_blocks", "from_blocks",
     "forward_int", "forward_scaled", "inverse", "reconstruct_zonal", "reconstruct_zonal_exact",
     "reconstruct_from_coef_exact", "round_u8_exact576",
@@ -93,6 +94,33 @@ def proposed_matrix() -> np.ndarray:
 def coarse_matrix() -> np.ndarray:
     """Coarse non-orthogonal approximation C_hat = 1/2 C0."""
     return 0.5 * c0_matrix().astype(np.float64)
+
+
+def roundoff_matrix(kind: str = "round", alpha: float = 2.0) -> np.ndarray:
+    """The paper's constructive family f(alpha C) (P:131-151 with f = round-off, alpha = 2) and the
+    generalisations the conclusion proposes, "usual floor and ceiling functions can be considered
+    instead of the round-off function", SURVEY §8(f) F4.  int64."""
+    f = {"round": round_half_away, "floor": np.floor, "ceil": np.ceil}[kind]
+    return np.asarray(f(alpha * dct_matrix()), dtype=np.float64).astype(np.int64)
+
+
+def polar_orthogonal(T: np.ndarray) -> np.ndarray:
+    """S . T with S = sqrt((T T^T)^-1) (principal root): the orthogonal polar factor of
+    an invertible T.  For T = C0 this is the proposed C_orth (S diagonal); for a general
+    round-off variant S is a dense symmetric matrix (no fast algorithm, F4)."""
+    T = np.asarray(T, dtype=np.float64)
+    return orthogonalizer(T) @ T
+
+
+def ceil_matrix() -> np.ndarray:
+    """F4 variant: the orthogonal polar factor of ceil(2 C).  ceil(2 C) has entries
+    in {0, 1} and is invertible (det 16); its Gram matrix is not diagonal, so S is dense."""
+    return polar_orthogonal(roundoff_matrix("ceil"))
+
+
+def sdct_sign_matrix() -> np.ndarray:
+    """sign(C) (int64, entries +-1): the SDCT comparator is sign(C) / (2 sqrt 2) (R11)."""
+    return np.sign(dct_matrix()).astype(np.int64)
 
 
 def frobenius_optimal_scale() -> float:

@@ -3,7 +3,7 @@
 Python surface = the C ABI in include/adct.h (same names, argument marshalling only):
 forward, inverse, compress_psnr, psnr, compress_psnr_host.  See DESIGN.md.
 """
-from ._lib import (AdctError, compress_psnr, compress_psnr_dense, compress_psnr_host, compress_psnr_multi,  # noqa: F401
+from ._lib import (AdctError, compress_psnr, compress_psnr_dense, compress_psnr_sdct, compress_psnr_host, compress_psnr_multi,  # noqa: F401
                    compress_sse576,
                    diag_energy,
                    empty_plane, sweep_psnr,
@@ -12,5 +12,5 @@ from ._lib import (AdctError, compress_psnr, compress_psnr_dense, compress_psnr_
 
 __all__ = ["forward", "inverse", "compress_psnr", "psnr", "compress_psnr_host", "load", "launch_count",
            "version", "AdctError", "empty_plane", "to_device", "quant_reciprocals",
-           "compress_psnr_dense", "transform_matrix", "diag_energy", "sweep_psnr", "uqi", "compress_psnr_multi",
+           "compress_psnr_dense", "compress_psnr_sdct", "transform_matrix", "diag_energy", "sweep_psnr", "uqi", "compress_psnr_multi",
            "compress_sse576"]

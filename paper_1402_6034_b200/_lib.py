@@ -27,7 +27,7 @@ SIGNATURES = {
                                   _vp, _vp]),
     "adct_psnr": (_i32, [_vp, _i64, _i64, _vp, _vp]),
     "adct_compress_psnr_host": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _i32, _f32, _vp, _i64,
-                                       _vp, _vp, _vp]),
+                                       _vp, _vp, _vp, _vp]),
     "adct_compress_psnr_multi": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _i32, _vp, _vp]),
     "adct_compress_sse576": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _vp, _vp]),
     "adct_quant_reciprocals": (_i32, [_f32, _vp]),
@@ -36,6 +36,7 @@ SIGNATURES = {
     "adct_uqi": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp]),
     "adct_transform_matrix": (_i32, [_i32, _vp]),
     "adct_diag_energy": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp]),
+    "adct_compress_psnr_sdct": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _vp]),
     "adct_sweep_psnr": (_i32, [_vp, _i64, _i64, _vp, _i32, _vp, _vp, _vp]),
     "adct_status_string": (ctypes.c_char_p, [_i32]),
     "adct_last_cuda_error": (_i32, []),
@@ -120,7 +121,7 @@ def to_device(x, device="cuda"):
     return out
 
 
-TRANSFORMS = {"proposed": 0, "dct": 1, "sdct": 2, "coarse": 3, "custom": 4}
+TRANSFORMS = {"proposed": 0, "dct": 1, "sdct": 2, "coarse": 3, "custom": 4, "ceil": 5}
 
 
 def transform_matrix(kind: str) -> np.ndarray:
@@ -151,6 +152,18 @@ def compress_psnr_dense(x, r: int, transform: str = "dct", matrix=None, sse=None
                                            cm.ctypes.data if cm is not None else None, rp, rpitch, ristr,
                                            sse.data_ptr(), _stream(stream)), "adct_compress_psnr_dense")
     return (sse, recon_out) if recon else sse
+
+
+def compress_psnr_sdct(x, r: int, sse=None, stream=None):
+    """adct_compress_psnr_sdct: the SDCT comparator on the integer fast path (24-add butterflies),
+    per-image SSE (float64 [n], device)."""
+    torch = _torch()
+    p, n, h, w, pitch, istr = _plane(x, 1)
+    if sse is None:
+        sse = torch.empty((n,), dtype=torch.float64, device=x.device)
+    _check(load().adct_compress_psnr_sdct(p, n, h, w, pitch, istr, int(r), sse.data_ptr(), _stream(stream)),
+           "adct_compress_psnr_sdct")
+    return sse
 
 
 def uqi(x, y, out=None, stream=None):
@@ -306,10 +319,11 @@ def psnr(sse, pixels: int, out=None, stream=None):
 
 
 def compress_psnr_host(host_images, r_list, q: float = 0.0, dev_buf=None, dev_sse=None, host_psnr=None,
-                       stream=None):
+                       stream=None, copy_stream=None):
     """adct_compress_psnr_host: end-to-end from host memory (pinned torch uint8 [n, h, w] or numpy).
 
-    Returns host PSNR [len(r_list), n] (float64, valid after the stream is synchronised).
+    copy_stream: an optional torch.cuda.Stream for the overlapped (double-buffered) host->device
+    copies.  Returns host PSNR [len(r_list), n] (float64, valid after the stream is synchronised).
     """
     torch = _torch()
     if isinstance(host_images, np.ndarray):
@@ -328,8 +342,9 @@ def compress_psnr_host(host_images, r_list, q: float = 0.0, dev_buf=None, dev_ss
     if host_psnr is None:
         host_psnr = torch.empty((nr, n), dtype=torch.float64, pin_memory=True)
     rl = (ctypes.c_int * nr)(*[int(v) for v in r_list])
+    cs = ctypes.c_void_p(copy_stream.cuda_stream) if copy_stream is not None else None
     _check(load().adct_compress_psnr_host(host_images.data_ptr(), n, h, w, host_images.stride(1),
                                           host_images.stride(0), rl, nr, float(q), dev_buf.data_ptr(),
                                           dev_buf.numel(), dev_sse.data_ptr(), host_psnr.data_ptr(),
-                                          _stream(stream)), "adct_compress_psnr_host")
+                                          _stream(stream), cs), "adct_compress_psnr_host")
     return host_psnr

@@ -345,7 +345,7 @@ const char* adct_status_string(adct_status s) {
 }
 
 int adct_last_cuda_error(void) { return g_last_cuda; }
-int adct_version(void) { return 10000; }
+int adct_version(void) { return 10100; }
 int64_t adct_launch_count(void) { return g_launches; }
 
 adct_status adct_forward(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
@@ -570,9 +570,84 @@ adct_status adct_compress_sse576(const uint8_t* src, int64_t n, int64_t h, int64
   return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
 }
 
+// Symmetric 8x8 eigendecomposition by cyclic Jacobi rotations (host, double): A = V diag(w) V^T.
+static void jacobi8(const double* Ain, double* w, double* V) {
+  double A[64];
+  for (int i = 0; i < 64; ++i) {
+    A[i] = Ain[i];
+    V[i] = (i % 9 == 0) ? 1.0 : 0.0;
+  }
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (int i = 0; i < 8; ++i)
+      for (int j = i + 1; j < 8; ++j) off += A[i * 8 + j] * A[i * 8 + j];
+    if (off < 1e-30) break;
+    for (int p = 0; p < 8; ++p)
+      for (int q = p + 1; q < 8; ++q) {
+        const double apq = A[p * 8 + q];
+        if (fabs(apq) < 1e-300) continue;
+        const double th = (A[q * 8 + q] - A[p * 8 + p]) / (2.0 * apq);
+        const double tt = (th >= 0 ? 1.0 : -1.0) / (fabs(th) + sqrt(th * th + 1.0));
+        const double c = 1.0 / sqrt(tt * tt + 1.0), sn = tt * c;
+        for (int k = 0; k < 8; ++k) {  // A <- J^T A J
+          const double akp = A[k * 8 + p], akq = A[k * 8 + q];
+          A[k * 8 + p] = c * akp - sn * akq;
+          A[k * 8 + q] = sn * akp + c * akq;
+        }
+        for (int k = 0; k < 8; ++k) {
+          const double apk = A[p * 8 + k], aqk = A[q * 8 + k];
+          A[p * 8 + k] = c * apk - sn * aqk;
+          A[q * 8 + k] = sn * apk + c * aqk;
+        }
+        for (int k = 0; k < 8; ++k) {
+          const double vkp = V[k * 8 + p], vkq = V[k * 8 + q];
+          V[k * 8 + p] = c * vkp - sn * vkq;
+          V[k * 8 + q] = sn * vkp + c * vkq;
+        }
+      }
+  }
+  for (int i = 0; i < 8; ++i) w[i] = A[i * 9];
+}
+
+// Orthogonal polar factor (T T^T)^(-1/2) T of an invertible T (F4 for ceil(2C)).
+static bool polar_factor(const double* T, double* out) {
+  double G[64], w[8], V[64], S[64];
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) {
+      double a = 0.0;
+      for (int k = 0; k < 8; ++k) a += T[i * 8 + k] * T[j * 8 + k];
+      G[i * 8 + j] = a;
+    }
+  jacobi8(G, w, V);
+  for (int i = 0; i < 8; ++i)
+    if (!(w[i] > 1e-12)) return false;  // singular (e.g. floor(2C): a zero row)
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) {
+      double a = 0.0;
+      for (int k = 0; k < 8; ++k) a += V[i * 8 + k] * V[j * 8 + k] / sqrt(w[k]);
+      S[i * 8 + j] = a;
+    }
+  for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 8; ++j) {
+      double a = 0.0;
+      for (int k = 0; k < 8; ++k) a += S[i * 8 + k] * T[k * 8 + j];
+      out[i * 8 + j] = a;
+    }
+  return true;
+}
+
 // The library's own matrices (independent of the CPU oracle): exact DCT-II from cos, C0 = [2C]
-// with Matlab rounding, S from diag(C0 C0^T)^(-1/2), SDCT = sign(C)/(2 sqrt 2), coarse = C0 / 2.
+// with Matlab rounding, S from diag(C0 C0^T)^(-1/2), SDCT = sign(C)/(2 sqrt 2), coarse = C0 / 2,
+// ceil variant = polar factor of ceil(2C) (F4).
 static void build_matrix(adct_transform_t t, double* M) {
+  if (t == ADCT_T_CEIL) {
+    double T[64];
+    for (int m = 0; m < 8; ++m)
+      for (int n = 0; n < 8; ++n)
+        T[m * 8 + n] = ceil(2.0 * (m == 0 ? 1.0 / (2.0 * sqrt(2.0)) : 0.5) * cos((2 * n + 1) * m * 3.14159265358979323846 / 16.0));
+    polar_factor(T, M);  // ceil(2C) is invertible (det 16)
+    return;
+  }
   const double PI = 3.14159265358979323846;
   double C[64];
   for (int m = 0; m < 8; ++m)
@@ -599,7 +674,7 @@ static void build_matrix(adct_transform_t t, double* M) {
 }
 
 adct_status adct_transform_matrix(adct_transform_t t, double* out) {
-  if (!out || t < ADCT_T_PROPOSED || t > ADCT_T_COARSE) return ADCT_EINVAL;
+  if (!out || t < ADCT_T_PROPOSED || t == ADCT_T_CUSTOM || t > ADCT_T_CEIL) return ADCT_EINVAL;
   build_matrix(t, out);
   return ADCT_OK;
 }
@@ -611,7 +686,7 @@ adct_status adct_compress_psnr_dense(const uint8_t* src, int64_t n, int64_t h, i
   adct_status st = check_geom(n, h, w);
   if (st) return st;
   if (r < 1 || r > 64 || !sse) return ADCT_EINVAL;
-  if (t < ADCT_T_PROPOSED || t > ADCT_T_CUSTOM || (t == ADCT_T_CUSTOM && !custom)) return ADCT_EINVAL;
+  if (t < ADCT_T_PROPOSED || t > ADCT_T_CEIL || (t == ADCT_T_CUSTOM && !custom)) return ADCT_EINVAL;
   if ((st = check_plane(src, h, w, pitch, img_stride))) return st;
   if (recon && (st = check_plane(recon, h, w * 4, recon_pitch, recon_img_stride))) return st;
   if ((uintptr_t)sse & 7u) return ADCT_EALIGN;
@@ -662,6 +737,39 @@ adct_status adct_compress_psnr_dense(const uint8_t* src, int64_t n, int64_t h, i
   cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(double) * (size_t)n, s);
   if (e != cudaSuccess) return cuda_fail(e);
   if ((st = launch_tma_kernel(k_compress_dense<0>, map, p, p.tiles, s))) return st;
+  return fx_finish(sse, n, fxk, s);
+}
+
+adct_status adct_compress_psnr_sdct(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                                    int64_t img_stride, int r, double* sse, adct_stream_t stream) {
+  adct_status st = check_geom(n, h, w);
+  if (st) return st;
+  if (r < 1 || r > 64 || !sse) return ADCT_EINVAL;
+  if ((st = check_plane(src, h, w, pitch, img_stride))) return st;
+  if ((uintptr_t)sse & 7u) return ADCT_EALIGN;
+  CUtensorMap map;
+  if ((st = make_u8_map(&map, src, n, h, w, pitch, img_stride))) return st;
+  CompressParams p;
+  memset(&p, 0, sizeof(p));
+  p.h16magic = 0x64646464u;
+  p.geo = make_geo(h, w);
+  p.tiles = p.geo.per_img * n;
+  p.h = (int)h;
+  p.w = (int)w;
+  p.sse = sse;
+  for (int k = 0; k < 8; ++k)
+    for (int l = 0; l < 8; ++l) {
+      const float m = zz_host(k, l) < r ? 1.f : 0.f;  // M_r as 0 / 1 weights (Z = Y / 8 folded in the 1/64)
+      p.tab.w[k * 8 + l] = make_float2(m, m);
+      p.tab.c[k * 8 + l] = make_float2(-KF * m, -KF * m);
+    }
+  // the SDCT is not orthogonal: |x^| <= |R| / 64 <= 64 * 16320 / 64, so (x - x^)^2 < 2^28 per pixel
+  const int fxk = fx_exponent(h * w, 28);
+  p.fx_scale = ldexp(1.0, fxk);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(double) * (size_t)n, s);
+  if (e != cudaSuccess) return cuda_fail(e);
+  if ((st = launch_tma_kernel(k_compress_sdct<0>, map, p, p.tiles, s, 2))) return st;
   return fx_finish(sse, n, fxk, s);
 }
 
@@ -763,16 +871,14 @@ adct_status adct_psnr(const double* sse, int64_t count, int64_t pixels, double* 
   return e == cudaSuccess ? ADCT_OK : cuda_fail(e);
 }
 
-adct_status adct_compress_psnr_multi(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
-                                     int64_t img_stride, const int* r_list, int n_r, double* sse,
-                                     adct_stream_t stream) {
-  adct_status st = check_geom(n, h, w);
-  if (st) return st;
-  if (!r_list || n_r < 1 || n_r > 64 || !sse) return ADCT_EINVAL;
-  for (int k = 0; k < n_r; ++k)
-    if (r_list[k] < 1 || r_list[k] > 64) return ADCT_EINVAL;
-  if ((st = check_plane(src, h, w, pitch, img_stride))) return st;
-  if ((uintptr_t)sse & 7u) return ADCT_EALIGN;
+}  // extern "C"
+
+namespace {
+// adct_compress_psnr_multi with the per-r rows `sse_stride` doubles apart (the host entry writes
+// chunks of images into columns of its [n_r][n] buffer).  Validation done by the callers.
+adct_status compress_multi_strided(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                                   int64_t img_stride, const int* r_list, int n_r, double* sse, int64_t sse_stride,
+                                   cudaStream_t s) {
   // the compiled set (BASELINE C5's r, any order, each once) -> one fused kernel
   int rowmap[8];
   bool fused = (n_r == RSetC5::n);
@@ -783,11 +889,11 @@ adct_status adct_compress_psnr_multi(const uint8_t* src, int64_t n, int64_t h, i
     fused = hit >= 0;
     rowmap[k] = hit;
   }
-  cudaStream_t s = (cudaStream_t)stream;
+  adct_status st = ADCT_OK;
   if (!fused) {  // any other set: independent passes
     for (int k = 0; k < n_r; ++k)
       if ((st = adct_compress_psnr(src, n, h, w, pitch, img_stride, r_list[k], 0.f, nullptr, ADCT_RECON_NONE, 0, 0,
-                                   sse + (int64_t)k * n, stream)))
+                                   sse + (int64_t)k * sse_stride, s)))
         return st;
     return ADCT_OK;
   }
@@ -801,12 +907,14 @@ adct_status adct_compress_psnr_multi(const uint8_t* src, int64_t n, int64_t h, i
   p.h = (int)h;
   p.w = (int)w;
   p.sse = sse;
-  p.sse_stride = n;
+  p.sse_stride = sse_stride;
   for (int k = 0; k < 8; ++k) p.rowmap[k] = rowmap[k];
   fill_zonal_tables(p.tab, 64);  // per-class weights (the compile-time masks need nothing else)
   const int fxk = fx_exponent(h * w, FX_BOUND_SSE);
   p.fx_scale = ldexp(1.0, fxk);
-  cudaError_t e = cudaMemsetAsync(sse, 0, sizeof(double) * (size_t)(n * n_r), s);
+  cudaError_t e = sse_stride == n ? cudaMemsetAsync(sse, 0, sizeof(double) * (size_t)(n * n_r), s)
+                                  : cudaMemset2DAsync(sse, sizeof(double) * (size_t)sse_stride, 0,
+                                                      sizeof(double) * (size_t)n, (size_t)n_r, s);
   if (e != cudaSuccess) return cuda_fail(e);
 #ifndef ADCT_SWEEP_INC
 #define ADCT_SWEEP_INC 1
@@ -818,16 +926,33 @@ adct_status adct_compress_psnr_multi(const uint8_t* src, int64_t n, int64_t h, i
     st = launch_compress(multi_kernel_c5(), 1, map, p, s);
   }
   if (st) return st;
-  return fx_finish(sse, n * n_r, fxk, s);
+  for (int k = 0; k < n_r && st == ADCT_OK; ++k) st = fx_finish(sse + (int64_t)k * sse_stride, n, fxk, s);
+  return st;
+}
+}  // namespace
+
+extern "C" {
+
+adct_status adct_compress_psnr_multi(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                                     int64_t img_stride, const int* r_list, int n_r, double* sse,
+                                     adct_stream_t stream) {
+  adct_status st = check_geom(n, h, w);
+  if (st) return st;
+  if (!r_list || n_r < 1 || n_r > 64 || !sse) return ADCT_EINVAL;
+  for (int k = 0; k < n_r; ++k)
+    if (r_list[k] < 1 || r_list[k] > 64) return ADCT_EINVAL;
+  if ((st = check_plane(src, h, w, pitch, img_stride))) return st;
+  if ((uintptr_t)sse & 7u) return ADCT_EALIGN;
+  return compress_multi_strided(src, n, h, w, pitch, img_stride, r_list, n_r, sse, n, (cudaStream_t)stream);
 }
 
 adct_status adct_compress_psnr_host(const uint8_t* host_src, int64_t n, int64_t h, int64_t w,
                                     int64_t host_pitch, int64_t host_img_stride, const int* r_list, int n_r,
                                     float q, uint8_t* dev_buf, int64_t dev_buf_bytes, double* dev_sse,
-                                    double* host_psnr, adct_stream_t stream) {
+                                    double* host_psnr, adct_stream_t stream, adct_stream_t copy_stream) {
   adct_status st = check_geom(n, h, w);
   if (st) return st;
-  if (!host_src || !r_list || n_r < 1 || !dev_buf || !dev_sse || !host_psnr) return ADCT_EINVAL;
+  if (!host_src || !r_list || n_r < 1 || n_r > 64 || !dev_buf || !dev_sse || !host_psnr) return ADCT_EINVAL;
   if (host_pitch < w || host_img_stride < h * host_pitch) return ADCT_EINVAL;
   for (int k = 0; k < n_r; ++k)
     if (r_list[k] < 1 || r_list[k] > 64) return ADCT_EINVAL;
@@ -847,7 +972,10 @@ adct_status adct_compress_psnr_host(const uint8_t* host_src, int64_t n, int64_t 
                             (size_t)host_pitch, (size_t)w, (size_t)h, cudaMemcpyHostToDevice, cs);
     return e;
   };
+  // zonal passes: the fused multi-r kernel when the set is BASELINE C5's (one read, one forward per
+  // tile for all r), independent passes otherwise; the quantiser: one pass per r
   auto compress_chunk = [&](const uint8_t* buf, int64_t i0, int64_t m) -> adct_status {
+    if (q == 0.f) return compress_multi_strided(buf, m, h, w, dpitch, dimg, r_list, n_r, dev_sse + i0, n, s);
     for (int k = 0; k < n_r; ++k) {
       adct_status st2 = adct_compress_psnr(buf, m, h, w, dpitch, dimg, r_list[k], q, nullptr, ADCT_RECON_NONE, 0,
                                            0, dev_sse + (int64_t)k * n + i0, stream);
@@ -855,14 +983,16 @@ adct_status adct_compress_psnr_host(const uint8_t* host_src, int64_t n, int64_t 
     }
     return ADCT_OK;
   };
-  // Double-buffered pipeline: the host->device copy of chunk c+1 (own stream) overlaps the
-  // compress passes of chunk c (caller's stream).  Chunks of about n/8 images, two per buffer.
   const int64_t half = cap / 2;
-  if (n >= 2 && half >= 1) {
+  cudaStream_t cs = (cudaStream_t)copy_stream;
+  if (cs && cs != s && n >= 2 && half >= 1) {
+    // Double-buffered pipeline on the caller's copy stream: the host->device copy of chunk c+1
+    // overlaps the passes of chunk c.  Chunks of about n/8 images, two per buffer; ordering by
+    // events (cheap to create; no stream is created), so the whole call can also be captured into
+    // a CUDA graph (fork / join through the events).
     const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(half, (n + 7) / 8));
-    cudaStream_t cs = nullptr;
     cudaEvent_t ready[2] = {nullptr, nullptr}, freed[2] = {nullptr, nullptr}, start = nullptr;
-    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    cudaError_t e = cudaSuccess;
     for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
       e = cudaEventCreateWithFlags(&ready[b], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&freed[b], cudaEventDisableTiming);
@@ -884,16 +1014,15 @@ adct_status adct_compress_psnr_host(const uint8_t* host_src, int64_t n, int64_t 
       if (e == cudaSuccess) st2 = compress_chunk(buf, i0, m);
       if (e == cudaSuccess && st2 == ADCT_OK) e = cudaEventRecord(freed[b], s);
     }
-    // resources are released once their pending work completes (no host synchronisation)
+    // events are released once their pending work completes (no host synchronisation)
     for (int b = 0; b < 2; ++b) {
       if (ready[b]) cudaEventDestroy(ready[b]);
       if (freed[b]) cudaEventDestroy(freed[b]);
     }
     if (start) cudaEventDestroy(start);
-    if (cs) cudaStreamDestroy(cs);
     if (e != cudaSuccess) return cuda_fail(e);
     if (st2) return st2;
-  } else {
+  } else {  // copies and passes alternate on the caller's stream
     for (int64_t i0 = 0; i0 < n; i0 += cap) {
       const int64_t m = std::min<int64_t>(cap, n - i0);
       cudaError_t e = stage(dev_buf, i0, m, s);

@@ -228,22 +228,22 @@ constexpr int recon_stage_bytes(int RECON) { return RECON == REC_F32 ? 4 * TILE_
 // ------------------------------------------------------------------------------------------
 
 // Forward half: packed SWAR coefficients Y (bias 0x80008000) of the two blocks of this lane.
-template <int R, int MODE>
+template <int R, int MODE, bool MIRB = false>
 __device__ __forceinline__ void compress_fwd(const uint8_t* tile, int lane, uint32_t (&Y)[8][8]) {
   constexpr int RF = R;  // forward pruning level (RT: runtime mask, all positions live)
   uint32_t P[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
-    pack_rows(lds64(tile + i * TILE_W + lane * 8), lds64(tile + (i + 8) * TILE_W + lane * 8), P[i]);
+    pack_rows_t<MIRB>(lds64(tile + i * TILE_W + lane * 8), lds64(tile + (i + 8) * TILE_W + lane * 8), P[i]);
   fwd2d<BIAS2, RF>(P, Y);
 }
 // ... and the row pass H of the columns in SKIP (their column pass is skipped)
-template <int R, int SKIP>
+template <int R, int SKIP, bool MIRB = false>
 __device__ __forceinline__ void compress_fwd_h(const uint8_t* tile, int lane, uint32_t (&Y)[8][8], uint32_t (&H)[8][8]) {
   uint32_t P[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
-    pack_rows(lds64(tile + i * TILE_W + lane * 8), lds64(tile + (i + 8) * TILE_W + lane * 8), P[i]);
+    pack_rows_t<MIRB>(lds64(tile + i * TILE_W + lane * 8), lds64(tile + (i + 8) * TILE_W + lane * 8), P[i]);
   fwd2d<BIAS2, R, SKIP>(P, Y, H);
 }
 
@@ -283,11 +283,12 @@ template <int N> __device__ __forceinline__ float2 err_fh(uint32_t ha, uint32_t 
   return err_fh<N, true>(ha, hb, r.v);
 }
 
-template <int R, int MODE, int RECON, int F16 = 0, bool GROUPED = false, bool STAGE = false>
+template <int R, int MODE, int RECON, int F16 = 0, bool GROUPED = false, bool STAGE = false, bool MIRB = false>
 __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const uint8_t* tile, int lane,
                                                const CompressParams& p, int img, int ty, int tx,
                                                uint8_t* sbuf = nullptr) {
   constexpr int RF = R;
+  static_assert(!MIRB || RECON == REC_NONE, "mirrored block B: SSE only (the reconstruction would be mirrored)");
   static_assert(F16 == 0 || (MODE == MODE_ZONAL && RECON == REC_NONE && RF < RT), "f16 error route: zonal SSE only");
   float2 V[64];
   static_for<64>([&](auto KLc) {
@@ -333,15 +334,19 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
       constexpr int N = decltype(Nc)::value;
       if constexpr (I < F16) {
         // f16 pairs (1024 + x_n, 1024 + x_{n+1}) of blocks A and B, one PRMT each per two pixels
+        // (MIRB: B's output column n is its pixel 7 - n: the pair (x_{7-n}, x_{6-n}))
         constexpr uint32_t sel = ((N >> 1) & 1) ? 0x4342u : 0x4140u;
+        constexpr uint32_t selb = MIRB ? (((N >> 1) & 1) ? 0x4041u : 0x4243u) : sel;
         const uint32_t ha = __byte_perm(N < 4 ? wa.x : wa.y, p.h16magic, sel);
-        const uint32_t hb = __byte_perm(N < 4 ? wb.x : wb.y, p.h16magic, sel);
+        const uint32_t hb = __byte_perm((N < 4) != MIRB ? wb.x : wb.y, p.h16magic, selb);
         const float2 e = err_fh<N>(ha, hb, get<N>(row));  // R' - 576 (1024 + x) = R - 576 x, exact
         acc[N] = f2fma(e, e, acc[N]);
       } else {
         // ZONAL: 576 x - R, exact integers; QUANT: x - x^ (fp32, irrational weights)
-        const float2 y = (MODE == MODE_ZONAL) ? px576b<(F16 > 0)>(N < 4 ? wa.x : wa.y, N < 4 ? wb.x : wb.y, N & 3)
-                                              : px1(N < 4 ? wa.x : wa.y, N < 4 ? wb.x : wb.y, N & 3);
+        constexpr int NB = MIRB ? 7 - N : N;  // block B's pixel in output column N
+        const float2 y = (MODE == MODE_ZONAL)
+                             ? px576b2<(F16 > 0)>(N < 4 ? wa.x : wa.y, NB < 4 ? wb.x : wb.y, N & 3, NB & 3)
+                             : px1(N < 4 ? wa.x : wa.y, N < 4 ? wb.x : wb.y, N & 3);
         const float2 e = rsub(y, get<N>(row));
         acc[N] = f2fma(e, e, acc[N]);
         if constexpr (RECON != REC_NONE) xr[N] = val(get<N>(row));
@@ -539,7 +544,8 @@ template <int R, int MODE, int RECON, int ST = compress_stages(R),
                      : ((MODE == MODE_QUANT && RECON == REC_NONE && R == 64) ? ADCT_MINB_QRES : ADCT_MINB_RT),
           bool RES = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT && compress_resid_r(R)),
           int F16 = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_f16_rows(R) : 0,
-          bool GRP = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_grouped(R) : false>
+          bool GRP = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_grouped(R) : false,
+          bool MIRB = ADCT_MIRB && RECON == REC_NONE && ((MODE == MODE_ZONAL && R < RT) || (MODE == MODE_QUANT && R == 64))>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     k_compress(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CompressParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -568,18 +574,18 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     if constexpr (RES) {
       if constexpr (ADCT_RESID_HC && hcol_mask(R) != 0 && !GRP) {
         uint32_t H[8][8];
-        compress_fwd_h<RESID + R, hcol_mask(R)>(tile, lane, Y, H);
+        compress_fwd_h<RESID + R, hcol_mask(R), MIRB>(tile, lane, Y, H);
         e2 = compress_resid_hc<R>(Y, H, p);
       } else {
-        compress_fwd<RESID + R, MODE>(tile, lane, Y);
+        compress_fwd<RESID + R, MODE, MIRB>(tile, lane, Y);
         e2 = compress_resid<R, GRP>(Y, p);
       }
     } else if constexpr (MODE == MODE_QUANT && RECON == REC_NONE && R == 64) {
-      compress_fwd<64, MODE>(tile, lane, Y);
+      compress_fwd<64, MODE, MIRB>(tile, lane, Y);
       e2 = compress_quant_resid(Y, p);
     } else {
-      compress_fwd<R, MODE>(tile, lane, Y);
-      e2 = compress_inv<R, MODE, RECON, F16, GRP>(Y, tile, lane, p, img, ty, tx);
+      compress_fwd<R, MODE, MIRB>(tile, lane, Y);
+      e2 = compress_inv<R, MODE, RECON, F16, GRP, false, MIRB>(Y, tile, lane, p, img, ty, tx);
     }
     acc += fx_lane(e2, fxs);
   });
@@ -1579,6 +1585,140 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INC_MINB)
     for (int b = 0; b < NB; ++b) dacc[b] += fx_lane(acc[b], fxs);
   });
   flush();
+}
+
+// ------------------------------------------------------------------------------------------
+// SDCT comparator on the integer fast path (F4 "reusing the integer machinery with
+// a different T / D").  The SDCT is sign(C) / (2 sqrt 2) (reading R11) and its fast algorithm
+// costs 24 additions per 1-D transform (Table 1).  With T_s = sign(C) (entries +-1):
+//   Y = T_s X T_s^T (exact, |Y| <= 16320, the same packed 2 x int16 SWAR as the proposed forward),
+//   Z = Y / 8, X^ = T^T (M_r . Z) T = R / 64 with R = T_s^T (M_r . Y) T_s (exact in fp32, |R| < 2^21),
+//   e = 64 x - R per pixel (exact), SSE = sum e^2 / 4096.
+// The SDCT is not orthogonal: X^ is the paper's "approximate inversion" by the transpose.
+// Forward graph: a_n = x_n + x_{7-n}, b_n = x_n - x_{7-n}; even rows (+ + + +, + + - -, + - - +,
+// + - + -) on a as a 4-point Hadamard; odd rows (+ + + +, + - - -, + - + +, + - + -) on b with
+// t = b0 + b1, u = b0 - b1, v = b2 + b3, w = b2 - b3: X1 = t + v, X3 = u - v, X5 = u + v, X7 = u + w.
+// ------------------------------------------------------------------------------------------
+template <uint32_t K>
+__device__ __forceinline__ void fwd8_sdct(const uint32_t (&x)[8], uint32_t (&X)[8]) {
+  const uint32_t a0 = x[0] + x[7], a1 = x[1] + x[6], a2 = x[2] + x[5], a3 = x[3] + x[4];
+  const uint32_t b0 = x[0] - x[7], b1 = x[1] - x[6], b2 = x[2] - x[5], b3 = x[3] - x[4];
+  const uint32_t s01 = a0 + a1, d01 = a0 - a1, s23 = a2 + a3, d23 = a2 - a3;
+  const uint32_t t = b0 + b1, u = b0 - b1, v = b2 + b3, w = b2 - b3;
+  X[0] = s01 + s23 + K;
+  X[2] = s01 - s23 + K;
+  X[4] = d01 - d23 + K;
+  X[6] = d01 + d23 + K;
+  X[1] = t + v + K;
+  X[3] = u - v + K;
+  X[5] = u + v + K;
+  X[7] = u + w + K;
+}
+// x = T_s^T X (transposed graph, 24 additions) on typed f32x2 values
+template <class X0, class X1, class X2, class X3, class X4, class X5, class X6, class X7>
+__device__ __forceinline__ auto inv8_sdct(X0 x0, X1 x1, X2 x2, X3 x3, X4 x4, X5 x5, X6 x6, X7 x7) {
+  auto p = add(x0, x2), q = sub(x0, x2), r = add(x4, x6), s = sub(x4, x6);
+  auto a0 = add(p, r), a1 = sub(p, r), a2 = sub(q, s), a3 = add(q, s);
+  auto g = add(x1, x3), h = sub(x1, x3), i = add(x5, x7), j = sub(x5, x7);
+  auto b0 = add(g, i), b1 = sub(h, i), b2 = add(h, i), b3 = add(h, j);
+  return cuda::std::make_tuple(add(a0, b0), add(a1, b1), add(a2, b2), add(a3, b3), sub(a3, b3), sub(a2, b2),
+                               sub(a1, b1), sub(a0, b0));
+}
+// e for pixel N of row (A, B) = R' -/+ 64 (1024 + x) through the mixed-precision FMA (exact):
+// 0xD400 = f16(-64), 0x5400 = f16(+64)
+template <bool HI, bool NEG>
+__device__ __forceinline__ float fhfma64(uint32_t h2, float c) {
+  float d;
+  if constexpr (HI)
+    asm("{.reg .f16 a, b; mov.b32 {_, a}, %1; mov.b16 b, %3; fma.rn.f32.f16 %0, a, b, %2;}"
+        : "=f"(d) : "r"(h2), "f"(c), "n"(NEG ? 0x5400 : 0xD400));
+  else
+    asm("{.reg .f16 a, b; mov.b32 {a, _}, %1; mov.b16 b, %3; fma.rn.f32.f16 %0, a, b, %2;}"
+        : "=f"(d) : "r"(h2), "f"(c), "n"(NEG ? 0x5400 : 0xD400));
+  return d;
+}
+template <int N, bool NEG> __device__ __forceinline__ float2 err64(uint32_t ha, uint32_t hb, float2 v) {
+  return make_float2(fhfma64<(N & 1) != 0, NEG>(ha, v.x), fhfma64<(N & 1) != 0, NEG>(hb, v.y));
+}
+constexpr float DC_BIAS64 = 65536.0f;  // 64 * 1024: injected at the DC (T_s row 0 is all ones)
+
+template <int UNUSED = 0>
+__global__ void __launch_bounds__(WARPS * 32, ADCT_MINB_RT)
+    k_compress_sdct(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CompressParams p) {
+  constexpr int ST = 2;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  uint8_t* ring = smem + warp * (ST * TILE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * ST * TILE_BYTES) + warp * ST;
+  const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
+  const float fxs = (float)(p.fx_scale / 4096.0);  // e = 64 (x - x^)
+  int cur = -1;
+  long long acc = 0;
+  tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
+                      [&](const uint8_t* tile, int img, int ty, int tx) {
+    if (img != cur) {
+      const long long v = warp_sum_ll(acc);
+      if (lane == 0 && cur >= 0) fx_flush(p.sse + cur, v);
+      cur = img;
+      acc = 0;
+    }
+    uint32_t P[8][8], H[8][8], Y[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      pack_rows(lds64(tile + i * TILE_W + lane * 8), lds64(tile + (i + 8) * TILE_W + lane * 8), P[i]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) fwd8_sdct<0u>(P[i], H[i]);
+#pragma unroll
+    for (int l = 0; l < 8; ++l) {
+      uint32_t c[8], o[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) c[i] = H[i][l];
+      fwd8_sdct<BIAS2>(c, o);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) Y[k][l] = o[k];
+    }
+    float2 V[64];  // M_r . Y (runtime mask as 0 / 1 weights), DC biased by 64 * 1024 for the f16 route
+#pragma unroll
+    for (int kl = 0; kl < 64; ++kl)
+      V[kl] = f2fma(biased_pair(Y[kl / 8][kl % 8]), f2(p.tab.w[kl].x), f2(p.tab.c[kl].x + (kl == 0 ? DC_BIAS64 : 0.f)));
+    float2 a2[8];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) a2[n] = f2(0.f);
+    auto col = [&](auto Lc) {
+      constexpr int L = decltype(Lc)::value;
+      return inv8_sdct(FV<false>{V[0 * 8 + L]}, FV<false>{V[1 * 8 + L]}, FV<false>{V[2 * 8 + L]}, FV<false>{V[3 * 8 + L]},
+                       FV<false>{V[4 * 8 + L]}, FV<false>{V[5 * 8 + L]}, FV<false>{V[6 * 8 + L]}, FV<false>{V[7 * 8 + L]});
+    };
+    auto u0 = col(cuda::std::integral_constant<int, 0>{});
+    auto u1 = col(cuda::std::integral_constant<int, 1>{});
+    auto u2 = col(cuda::std::integral_constant<int, 2>{});
+    auto u3 = col(cuda::std::integral_constant<int, 3>{});
+    auto u4 = col(cuda::std::integral_constant<int, 4>{});
+    auto u5 = col(cuda::std::integral_constant<int, 5>{});
+    auto u6 = col(cuda::std::integral_constant<int, 6>{});
+    auto u7 = col(cuda::std::integral_constant<int, 7>{});
+    static_for<8>([&](auto Ic) {
+      constexpr int I = decltype(Ic)::value;
+      using cuda::std::get;
+      auto row = inv8_sdct(get<I>(u0), get<I>(u1), get<I>(u2), get<I>(u3), get<I>(u4), get<I>(u5), get<I>(u6), get<I>(u7));
+      const uint2 wa = lds64_reload(tile + I * TILE_W + lane * 8);
+      const uint2 wb = lds64_reload(tile + (I + 8) * TILE_W + lane * 8);
+      static_for<8>([&](auto Nc) {
+        constexpr int N = decltype(Nc)::value;
+        constexpr uint32_t sel = ((N >> 1) & 1) ? 0x4342u : 0x4140u;
+        const uint32_t ha = __byte_perm(N < 4 ? wa.x : wa.y, p.h16magic, sel);
+        const uint32_t hb = __byte_perm(N < 4 ? wb.x : wb.y, p.h16magic, sel);
+        const auto rv = get<N>(row);
+        const float2 e = err64<N, decltype(rv)::neg>(ha, hb, rv.v);  // R' - 64 (1024 + x) = R - 64 x, exact
+        a2[N] = f2fma(e, e, a2[N]);
+      });
+    });
+    const float2 s01 = f2add(a2[0], a2[1]), s23 = f2add(a2[2], a2[3]);
+    const float2 s45 = f2add(a2[4], a2[5]), s67 = f2add(a2[6], a2[7]);
+    acc += fx_lane(f2add(f2add(s01, s23), f2add(s45, s67)), fxs);
+  });
+  const long long v = warp_sum_ll(acc);
+  if (lane == 0 && cur >= 0) fx_flush(p.sse + cur, v);
 }
 
 typedef void (*CompressKernel)(CUtensorMap, CompressParams);

@@ -53,3 +53,30 @@ def inverse8(X, k: Counter):
     for n, (a, b) in enumerate(((a0, b0), (a1, b1), (a2, b2), (a3, b3))):
         x[n], x[7 - n] = k.add(a, b), k.sub(a, b)
     return x
+
+
+def sdct_forward8(x, k: Counter):
+    """X = sign(C) . x for the SDCT comparator (Table 1 P:288-289 "24 additions"): stage 1
+    (8 adds), even rows (+ + + +, + + - -, + - - +, + - + -) on a as a 4-point Hadamard (8 adds),
+    odd rows (+ + + +, + - - -, + - + +, + - + -) on b with shared b0 +- b1, b2 +- b3 (8 adds)."""
+    a = [k.add(x[n], x[7 - n]) for n in range(4)]
+    b = [k.sub(x[n], x[7 - n]) for n in range(4)]
+    s01, d01, s23, d23 = k.add(a[0], a[1]), k.sub(a[0], a[1]), k.add(a[2], a[3]), k.sub(a[2], a[3])
+    t, u, v, w = k.add(b[0], b[1]), k.sub(b[0], b[1]), k.add(b[2], b[3]), k.sub(b[2], b[3])
+    X = [None] * 8
+    X[0], X[2] = k.add(s01, s23), k.sub(s01, s23)
+    X[4], X[6] = k.sub(d01, d23), k.add(d01, d23)
+    X[1], X[3], X[5], X[7] = k.add(t, v), k.sub(u, v), k.add(u, v), k.add(u, w)
+    return X
+
+
+def sdct_inverse8(X, k: Counter):
+    """x = sign(C)^T . X (transposed graph): 8 + 8 + 8 = 24 adds."""
+    p, q, r, s = k.add(X[0], X[2]), k.sub(X[0], X[2]), k.add(X[4], X[6]), k.sub(X[4], X[6])
+    a = [k.add(p, r), k.sub(p, r), k.sub(q, s), k.add(q, s)]
+    g, h, i, j = k.add(X[1], X[3]), k.sub(X[1], X[3]), k.add(X[5], X[7]), k.sub(X[5], X[7])
+    b = [k.add(g, i), k.sub(h, i), k.add(h, i), k.add(h, j)]
+    x = [None] * 8
+    for n in range(4):
+        x[n], x[7 - n] = k.add(a[n], b[n]), k.sub(a[n], b[n])
+    return x

@@ -21,7 +21,7 @@ def header_functions():
 def test_library_exports_every_declared_symbol():
     lib = A.load()
     names = header_functions()
-    assert len(names) == 17
+    assert len(names) == 18
     for name in names:
         assert hasattr(lib, name), name
         assert name in _lib.SIGNATURES, name
@@ -92,7 +92,7 @@ def test_inverse_and_psnr_validation():
     assert lib.adct_psnr(16, 0, 64, 32, None) == E
     assert lib.adct_psnr(16, 4, 0, 32, None) == E
     rl = (ctypes.c_int * 2)(10, 70)
-    assert lib.adct_compress_psnr_host(16, 1, 8, 16, 16, 128, rl, 2, 0.0, 16, 4096, 64, 128, None) == E
+    assert lib.adct_compress_psnr_host(16, 1, 8, 16, 16, 128, rl, 2, 0.0, 16, 4096, 64, 128, None, None) == E
 
 
 def test_no_cpu_fallback():
@@ -122,8 +122,19 @@ def test_library_matrices_match_oracle():
     assert np.abs(A.transform_matrix("proposed") - O.proposed_matrix()).max() < 1e-15
     assert np.abs(A.transform_matrix("sdct") - O.sdct_matrix()).max() < 1e-15
     assert np.abs(A.transform_matrix("coarse") - O.coarse_matrix()).max() < 1e-15
+    # F4: the library's own Jacobi polar factor of ceil(2C) against the oracle's eigendecomposition
+    assert np.abs(A.transform_matrix("ceil") - O.ceil_matrix()).max() < 1e-13
     with pytest.raises(A.AdctError):
         A.transform_matrix("custom")
+
+
+def test_sdct_validation():
+    lib = A.load()
+    E = _lib.ADCT_EINVAL
+    assert lib.adct_compress_psnr_sdct(16, 1, 8, 16, 16, 128, 0, 64, None) == E    # r = 0
+    assert lib.adct_compress_psnr_sdct(16, 1, 8, 16, 16, 128, 65, 64, None) == E   # r = 65
+    assert lib.adct_compress_psnr_sdct(16, 1, 8, 16, 16, 128, 10, 0, None) == E    # sse NULL
+    assert lib.adct_compress_psnr_sdct(16, 1, 12, 16, 16, 192, 10, 64, None) == E  # h not a multiple of 8
 
 
 def test_dense_validation():

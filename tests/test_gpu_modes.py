@@ -194,3 +194,46 @@ def test_inverse_no_writes_outside_every_input_kind(n, h, w, coef):
             A.inverse(y, r=r, out=out, dst=win)
             assert torch.all(_outside(big, n, h, w) == fill), (coef, out, r)
     torch.cuda.synchronize()
+
+
+# ------------------------------------------------------------------ F1 SDCT fast path, F4 ceil variant
+
+def _comparator_images(h=64, w=96):
+    ii, jj = np.indices((h, w))
+    return np.concatenate([S.corpus_c2(3, h, w), rng.integers(0, 256, (2, h, w), dtype=np.uint8),
+                           (255 * ((ii + jj) % 2)).astype(np.uint8)[None], np.full((1, h, w), 255, np.uint8)])
+
+
+@pytest.mark.parametrize("r", [1, 2, 3, 5, 10, 21, 36, 50, 63, 64])
+def test_sdct_integer_fast_path_vs_oracle(r):
+    """adct_compress_psnr_sdct (24-add SWAR forward, transposed 24-add inverse, e = 64 x - R exact)
+    against the oracle's float64 pipeline with sign(C) / (2 sqrt 2) (R11): SSE within 1e-5."""
+    for h, w in ((64, 96), (40, 264)):
+        imgs = _comparator_images(h, w)
+        got = host(A.compress_psnr_sdct(dev(imgs), r))
+        want = O.compress_zonal_sse(imgs, r, O.sdct_matrix())
+        check_sse(got, want, h * w)
+
+
+def test_sdct_fast_path_matches_dense_and_c2_curve():
+    """C2 (45 x 512^2): the SDCT mean-PSNR curve from the integer fast path equals the oracle's, and
+    the fast path equals the dense fp32 comparator within the dense path's 1e-4."""
+    imgs = S.corpus_c2()
+    x = dev(imgs)
+    px = 512 * 512
+    for r in (1, 3, 6, 10, 15, 21, 28, 36, 45, 63):
+        fast = host(A.compress_psnr_sdct(x, r))
+        want = O.compress_zonal_sse(imgs, r, O.sdct_matrix())
+        check_sse(fast, want, px)
+        assert abs(O.mean_psnr(fast, px) - O.mean_psnr(want, px)) <= 1e-3
+        assert np.allclose(fast, host(A.compress_psnr_dense(x, r, "sdct")), rtol=1e-4)
+
+
+@pytest.mark.parametrize("r", [1, 3, 10, 21, 36, 50])
+def test_dense_ceil_variant_vs_oracle(r):
+    """F4: the polar factor of ceil(2C) (library's own Jacobi eigendecomposition) through the dense path
+    vs the oracle's float64 pipeline with O.ceil_matrix(); fp32 dense products: SSE rtol 1e-4."""
+    imgs = _comparator_images()
+    got = host(A.compress_psnr_dense(dev(imgs), r, "ceil"))
+    want = O.compress_zonal_sse(imgs, r, O.ceil_matrix())
+    check_sse(got, want, 64 * 96, rtol=1e-4)

@@ -429,15 +429,17 @@ def test_determinism_every_sum_entry():
     assert np.array_equal(u[0], u[1]) and np.array_equal(u[0], u[2])
 
 
-@pytest.mark.parametrize("n,buf_imgs", [(6, 2), (6, 1), (17, 5), (17, 17), (1, 3)])
-def test_end_to_end_host_entry_matches_device_path(n, buf_imgs):
-    # buf_imgs >= 2: double-buffered copy/compute pipeline (chunks of ~n/8 images, two buffers);
-    # buf_imgs == 1 or n == 1: copy and passes alternate on the caller's stream
+@pytest.mark.parametrize("n,buf_imgs,copy", [(6, 2, True), (6, 1, True), (17, 5, True), (17, 17, True), (1, 3, True),
+                                              (6, 2, False), (17, 5, False)])
+@pytest.mark.parametrize("rs", [[1, 3, 6, 10, 15, 21, 28, 36], [2, 10, 64]])
+def test_end_to_end_host_entry_matches_device_path(n, buf_imgs, copy, rs):
+    # copy stream and buf_imgs >= 2: double-buffered copy/compute pipeline (chunks of ~n/8 images, two
+    # buffers); buf_imgs == 1, n == 1 or no copy stream: copy and passes alternate on the caller's
+    # stream.  C5's r set runs the fused multi-r kernel, other sets independent passes.
     imgs = S.corpus_c2(n, 128, 128)
-    rs = [1, 3, 6, 10, 15, 21, 28, 36]
     pinned = torch.from_numpy(imgs).pin_memory()
     dev_buf = torch.empty((buf_imgs * 128 * 128,), dtype=torch.uint8, device="cuda")
-    ps = A.compress_psnr_host(pinned, rs, dev_buf=dev_buf)
+    ps = A.compress_psnr_host(pinned, rs, dev_buf=dev_buf, copy_stream=torch.cuda.Stream() if copy else None)
     torch.cuda.synchronize()
     for k, r in enumerate(rs):
         want_sse = O.compress_zonal_sse(imgs, r)

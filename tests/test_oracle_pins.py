@@ -62,6 +62,75 @@ def test_c0_is_not_orthogonal_and_coarse():
     assert np.allclose((O.coarse_matrix() ** 2).sum(axis=1), np.array([8, 6, 4, 6, 8, 6, 4, 6]) / 4.0)
 
 
+def _det_exact(M):
+    """Exact integer determinant (fraction-free Bareiss elimination, Python ints)."""
+    A_ = [[int(v) for v in row] for row in M]
+    n, sign, prev = len(A_), 1, 1
+    for k in range(n - 1):
+        if A_[k][k] == 0:
+            sw = next((i for i in range(k + 1, n) if A_[i][k] != 0), None)
+            if sw is None:
+                return 0
+            A_[k], A_[sw] = A_[sw], A_[k]
+            sign = -sign
+        for i in range(k + 1, n):
+            for j in range(k + 1, n):
+                A_[i][j] = (A_[i][j] * A_[k][k] - A_[i][k] * A_[k][j]) // prev
+        prev = A_[k][k]
+    return sign * A_[n - 1][n - 1]
+
+
+def test_F4_roundoff_family_pins():
+    """F4 ("floor and ceiling functions can be considered instead of the round-off
+    function"): the generic f(2 C) builder reproduces the printed C0 for f = round (and its polar
+    factor the printed S . C0); floor(2 C) is singular (its DC row 2/(2 sqrt 2) < 1 floors to 0), so it
+    has no orthogonalisation; ceil(2 C) has entries in {0, 1}, exact determinant 16 (Bareiss, no
+    floating point), a non-diagonal Gram matrix, and its polar factor is orthogonal with
+    S = (T T^T)^(-1/2) symmetric positive definite."""
+    assert np.array_equal(O.roundoff_matrix("round"), golden_c0())
+    assert np.allclose(O.polar_orthogonal(golden_c0()), O.proposed_matrix(), atol=1e-14)
+    Tf = O.roundoff_matrix("floor")
+    assert np.all(Tf[0] == 0) and _det_exact(Tf) == 0
+    with pytest.raises(Exception):
+        O.polar_orthogonal(Tf)
+    Tc = O.roundoff_matrix("ceil")
+    assert set(np.unique(Tc)) <= {0, 1}
+    assert _det_exact(Tc) == 16
+    G = Tc @ Tc.T
+    assert np.any(G - np.diag(np.diag(G)) != 0)
+    Cc = O.ceil_matrix()
+    assert np.abs(Cc @ Cc.T - np.eye(8)).max() <= 1e-12
+    S_ = O.orthogonalizer(Tc)
+    assert np.allclose(S_, S_.T, atol=1e-14) and np.all(np.linalg.eigvalsh(S_) > 0)
+    assert np.abs(S_ @ S_ @ G.astype(float) - np.eye(8)).max() <= 1e-12
+    # the polar factor is the closest orthogonal matrix to T (Frobenius), P:189-200: no random
+    # orthogonal matrix Q may come closer
+    g = np.random.default_rng(5)
+    for _ in range(200):
+        Q, _ = np.linalg.qr(g.normal(size=(8, 8)))
+        assert np.linalg.norm(Tc - Q) >= np.linalg.norm(Tc - Cc) - 1e-12
+
+
+def test_F1_sdct_sign_matrix_and_24_add_graph():
+    """SDCT comparator (Table 1 P:288-289 "24 additions"): sign(C) has entries +-1 only (no
+    entry of C is near 0), equals sdct_matrix() * 2 sqrt 2, and the host model of its fast graph
+    equals sign(C) . x (and the transposed graph sign(C)^T . X) on unit and random vectors with
+    exactly Table 1's 24 additions and no multiplications or shifts."""
+    from reference_butterfly import sdct_forward8, sdct_inverse8
+    T = O.sdct_sign_matrix()
+    assert set(np.unique(T)) == {-1, 1} and np.abs(O.dct_matrix()).min() > 0.09
+    assert np.allclose(T / (2 * math.sqrt(2)), O.sdct_matrix(), atol=1e-15)
+    want = [int(v) for v in read_golden("table1_sdct.txt")[0]]
+    vecs = [np.eye(8, dtype=np.int64)[i] for i in range(8)] + [rng.integers(-300, 300, 8) for _ in range(2000)]
+    for v in vecs:
+        k = Counter()
+        assert np.array_equal(np.array(sdct_forward8(list(v), k)), T @ v)
+        assert [k.adds, k.mults, k.shifts, k.adds + k.mults + k.shifts] == want
+        k = Counter()
+        assert np.array_equal(np.array(sdct_inverse8(list(v), k)), T.T @ v)
+        assert k.adds == 24
+
+
 def test_P4_frobenius_scale_0_3922():
     printed = float(read_golden("frobenius_scale.txt")[0][0])
     a = O.frobenius_optimal_scale()
