@@ -13,7 +13,7 @@ reaches, P:250-253).
 
 Citations: ``P:n`` = /root/reference/PAPER.md line n (LaTeX source of the
 paper); section names follow the paper.  Readings where the paper is silent
-or garbled are numbered R1..R12 and listed in DESIGN.md §3.
+or garbled are numbered R1..R19 and listed in DESIGN.md §3.
 
 Parity pins: every public function here is pinned by ``tests/test_oracle_pins.py``
 against values the paper prints (``tests/golden/``), closed forms, invariants

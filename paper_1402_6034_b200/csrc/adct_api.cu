@@ -313,7 +313,7 @@ adct_status compress_dispatch(const CUtensorMap& map, const CUtensorMap& omap, b
       return launch_tma2(k_compress_recon<MODE_QUANT, REC_F32>, map, omap, p, crec_smem_bytes(REC_F32), s);
     if (bulk) return launch_tma2(k_compress_recon<MODE_QUANT, REC_U8>, map, omap, p, crec_smem_bytes(REC_U8), s);
     if (recon_t == ADCT_RECON_NONE && r == 64)  // C4's case: compile-time mask, per-class constants
-      return launch_compress(k_compress<64, MODE_QUANT, REC_NONE>, 64, map, p, s);
+      return launch_compress(q < 4.f ? quant64_kernel<true>() : quant64_kernel<false>(), 64, map, p, s);
     if (recon_t == ADCT_RECON_NONE) return launch_compress(k_compress<RT, MODE_QUANT, REC_NONE>, RT, map, p, s);
     if (recon_t == ADCT_RECON_F32) return launch_compress(k_compress<RT, MODE_QUANT, REC_F32>, RT, map, p, s);
     return launch_compress(k_compress<RT, MODE_QUANT, REC_U8>, RT, map, p, s);

@@ -467,6 +467,13 @@ __device__ __forceinline__ void inv8w(const float2 (&v)[8], float2 (&o)[8]) {
   o[4] = f2fma(b3, f2(-QW_RO), a3);
 }
 
+// LO adds the low part of the reciprocal (y * lo): the residual of an exactly lossless coefficient
+// stays ~1e-13 for any q.  Without it rho carries |Y / (q sqrt dd)| * 2^-24 of rounding (<= 7.6e-6 for
+// the DC at q = 16; SSE relative error ~2e-6 on C4 frames) and the DC at q = 16 (1 / 128, a power
+// of two) stays exact, so P18's constant frames are still bit-exact; one FFMA2 (two register-read
+// cycles) less per coefficient pair.  The host picks LO for q < 4, where |Y / (q sqrt dd)| (up to
+// 16320 / (4 q)) makes that rounding visible at the SSE bar (adct_api.cu).
+template <bool LO>
 __device__ __forceinline__ float2 compress_quant_resid(const uint32_t (&Y)[8][8], const CompressParams& p) {
   float2 U[8][8];  // column pass outputs [row][col]
   static_for<8>([&](auto Lc) {
@@ -480,7 +487,10 @@ __device__ __forceinline__ float2 compress_quant_resid(const uint32_t (&Y)[8][8]
       // rho = Y / (q sqrt dd) - k with the reciprocal as hi + lo: y hi - k is exact-ish in the fma
       // (near cancellation), y lo restores the rest — a DC residual that is 0 in exact arithmetic
       // stays ~1e-13 instead of ~1e-7 (lossless blocks keep SSE ~ 0)
-      v[K] = f2fma(y, f2(p.tab.sql[c]), f2fma(y, f2(p.tab.sq[c]), make_float2(-k.x, -k.y)));
+      if constexpr (LO)
+        v[K] = f2fma(y, f2(p.tab.sql[c]), f2fma(y, f2(p.tab.sq[c]), make_float2(-k.x, -k.y)));
+      else
+        v[K] = f2fma(y, f2(p.tab.sq[c]), make_float2(-k.x, -k.y));
     });
     inv8w(v, o);
 #pragma unroll
@@ -545,7 +555,8 @@ template <int R, int MODE, int RECON, int ST = compress_stages(R),
           bool RES = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT && compress_resid_r(R)),
           int F16 = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_f16_rows(R) : 0,
           bool GRP = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_grouped(R) : false,
-          bool MIRB = ADCT_MIRB && RECON == REC_NONE && ((MODE == MODE_ZONAL && R < RT) || (MODE == MODE_QUANT && R == 64))>
+          bool MIRB = ADCT_MIRB && RECON == REC_NONE && ((MODE == MODE_ZONAL && R < RT) || (MODE == MODE_QUANT && R == 64)),
+          bool QLO = false>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     k_compress(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CompressParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -582,7 +593,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
       }
     } else if constexpr (MODE == MODE_QUANT && RECON == REC_NONE && R == 64) {
       compress_fwd<64, MODE, MIRB>(tile, lane, Y);
-      e2 = compress_quant_resid(Y, p);
+      e2 = compress_quant_resid<QLO>(Y, p);
     } else {
       compress_fwd<R, MODE, MIRB>(tile, lane, Y);
       e2 = compress_inv<R, MODE, RECON, F16, GRP, false, MIRB>(Y, tile, lane, p, img, ty, tx);
@@ -1722,6 +1733,11 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_MINB_RT)
 }
 
 typedef void (*CompressKernel)(CUtensorMap, CompressParams);
+// C4's quantiser kernel (compile-time r = 64, residual form) without / with the reciprocal's low part
+template <bool LO> constexpr CompressKernel quant64_kernel() {
+  return &k_compress<64, MODE_QUANT, REC_NONE, compress_stages(64), ADCT_MINB_QRES, false, 0, false,
+                     (bool)ADCT_MIRB, LO>;
+}
 CompressKernel multi_kernel_c5();  // k_compress_multi<RSetC5>, instantiated in multi_r.cu
 CompressKernel sweep_inc_kernel_c5();  // k_compress_sweep_inc, instantiated in multi_r.cu
 // zonal kernels k_compress<r, ZONAL, RECON_NONE>, instantiated in zonal_part*.cu (4 TUs)

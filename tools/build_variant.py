@@ -20,8 +20,10 @@ a, defs = ap.parse_known_args()
 B.build()
 out = os.path.join(B.ROOT, "tune_variants", a.name)
 os.makedirs(out, exist_ok=True)
-objs = []
-for src in B._sources():
+import concurrent.futures as cf  # noqa: E402
+
+
+def one(src):
     tu = os.path.basename(src)[:-3]
     if a.tu is None or tu in a.tu:
         obj = os.path.join(out, tu + ".o")
@@ -29,10 +31,13 @@ for src in B._sources():
         r = subprocess.run(cmd, capture_output=True, text=True)
         open(obj + ".log", "w").write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
         if r.returncode:
-            sys.exit(r.stderr[-3000:])
-        objs.append(obj)
-    else:
-        objs.append(os.path.join(B.BUILD, tu + ".o"))
+            raise RuntimeError(r.stderr[-3000:])
+        return obj
+    return os.path.join(B.BUILD, tu + ".o")
+
+
+with cf.ThreadPoolExecutor(8) as ex:
+    objs = list(ex.map(one, B._sources()))
 lib = os.path.join(B.ROOT, "tune_variants", f"libadct_{a.name}.so")
 subprocess.run([B.nvcc()] + B.ARCH + ["-shared", "-o", lib] + objs, check=True)
 print(lib)

@@ -17,6 +17,7 @@ template <int OP>
 __global__ void __launch_bounds__(128) kern(uint32_t* out, uint32_t seed, unsigned long long* cyc) {
   uint32_t r[CH];
   unsigned long long f[CH];
+  unsigned long long kk = ((unsigned long long)(seed & 0xffu | 0x3f000000u) << 32) | (seed & 0xffu | 0x3f000000u);
 #pragma unroll
   for (int c = 0; c < CH; ++c) {
     r[c] = seed * (threadIdx.x + 3 + 7 * c);
@@ -48,6 +49,13 @@ __global__ void __launch_bounds__(128) kern(uint32_t* out, uint32_t seed, unsign
       if (OP == 7) asm volatile("add.f32 %0, %0, %1;" : "+r"(r[c]) : "r"(r[c1]));
       // scalar FADD, live + immediate
       if (OP == 8) asm volatile("add.f32 %0, %0, 0f3F800000;" : "+r"(r[c]));
+      // FADD2 with one live pair + one SHARED live pair (the same register pair in every instruction:
+      // operand-reuse cache) interleaved with a one-register PRMT: 2 + 1 reads per 2 instructions
+      if (OP == 14) {
+        asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(f[c]) : "l"(kk));
+        asm volatile("prmt.b32 %0, %0, 0, 0x3210;" : "+r"(r[c]));
+      }
+      if (OP == 15) asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(f[c]) : "l"(kk));
       // FADD2 imm form interleaved with IADD3 3-live
       if (OP == 9) {
         asm volatile("add.rn.f32x2 %0, %0, %1;" : "+l"(f[c]) : "l"(0x3f8000003f800000ull));
@@ -108,6 +116,8 @@ int main() {
     run<12>("FADD2 ll + IADD3 3", 2, sms, cps);
     run<13>("FADD2 ll + IADD 1+imm", 2, sms, cps);
     run<9>("FADD2 imm + IADD3 3", 2, sms, cps);
+    run<15>("FADD2 live + shared pair", 1, sms, cps);
+    run<14>("FADD2 l+shared + PRMT 1", 2, sms, cps);
   }
   return 0;
 }

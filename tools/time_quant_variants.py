@@ -16,6 +16,9 @@ sys.path.insert(0, __ROOT__)
 from paper_1402_6034_b200 import _lib
 if __LIBV__ != "default":
     _lib.LIB_PATH = __LIBV__
+    # older builds may lack newer entries: bind only what the timing uses
+    _lib.SIGNATURES = {k: v for k, v in _lib.SIGNATURES.items()
+                       if k in ("adct_compress_psnr", "adct_psnr", "adct_status_string", "adct_last_cuda_error")}
 import paper_1402_6034_b200 as A
 from synth import images as S
 v = S.device_video(NFR, 4320, 7680, seed=0, device="cuda")
