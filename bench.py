@@ -110,6 +110,35 @@ def issue_roofline(tr, per_r_ms, tiles_per_launch, sm_mhz, dev):
             "note": "compute roofline of the same kernel: 1 warp-instr/clk/SMSP at the sampled SM clock"}
 
 
+def regread_roofline(per_r_ms, tiles_per_launch, sm_mhz, dev, quant_ms=None, quant_tiles=None):
+    """The binding compute resource of the fused compress kernels: register-file read
+    cycles.  Achieved = the static read cycles per tile of each r's kernel (profiles/r02_regread.json,
+    tools/sass_regread.py on the built objects) x tiles / measured launch time; peak = 1 read cycle per
+    clock per SM sub-partition (148 x 4) at the SM clock sampled in the timed region."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_regread.json")) as f:
+            rr = json.load(f)
+    except Exception:
+        return None
+    if not sm_mhz or not all(str(r) in rr["zonal"] for r in R_SET):
+        return None
+    import torch
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    peak = sms * 4 * sm_mhz * 1e6
+    cyc = [rr["zonal"][str(r)]["read_cycles"] for r in R_SET]
+    per = {str(r): c * tiles_per_launch / (t * 1e-3) / peak for r, c, t in zip(R_SET, cyc, per_r_ms)}
+    tot = sum(c * tiles_per_launch for c in cyc) / (sum(per_r_ms) * 1e-3)
+    out = {"bound": "register-file reads", "achieved": tot, "peak": peak, "unit": "read-cycles/s", "frac": tot / peak,
+           "per_r_frac": per,
+           # the HBM fraction each r could reach at 100 % of the read bound: (tiles / s at one read
+           # cycle per clock per SMSP) / (tiles / s at the measured HBM bandwidth, 4 KiB per tile)
+           "model_bound_of_hbm": {str(r): (peak / c) / (measured_peaks()[0] * 1e9 / 4096) for r, c in zip(R_SET, cyc)},
+           "source": "profiles/r02_regread.json (tools/sass_regread.py); microbench evidence profiles/r02_regbank_microbench.txt"}
+    if quant_ms and quant_tiles and rr.get("quant64"):
+        out["quant_c4_frac"] = rr["quant64"]["read_cycles"] * quant_tiles / (quant_ms * 1e-3) / peak
+    return out
+
+
 class ClockSampler:
     """Samples SM clock and throttle reasons with NVML during the timed region."""
 
@@ -331,6 +360,7 @@ def main():
                 "per_r_frac": {str(r): bytes_launch / (t * 1e-3) / 1e9 / peak for r, t in zip(R_SET, per_r)}}
     clocks = clk.summary()
     issue = issue_roofline(tr, per_r, n_loc * (H // 16) * (W // 256), clocks.get("sm_mhz"), dev)
+    regread = regread_roofline(per_r, n_loc * (H // 16) * (W // 256), clocks.get("sm_mhz"), dev)
 
     # ---- secondary (SURVEY F3 with the inverse, reported separately): fused multi-r kernel —
     # one read and one forward per tile, then every r's zonal step, inverse and per-pixel error
@@ -537,7 +567,7 @@ def main():
                                           f" sharded by image; one NCCL all-reduce of the per-image SSE)",
                            "l2": "inputs 64 GiB >> 126 MB L2 (no flush needed)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clocks, "issue_roofline": issue, "fwd_only_c3": fwd_only, "quant_c4": quant_c4, "parseval_sweep_f3": sweep,
+                "clocks": clocks, "issue_roofline": issue, "regread_roofline": regread, "fwd_only_c3": fwd_only, "quant_c4": quant_c4, "parseval_sweep_f3": sweep,
                 "fused_multi_r_c5": fused, "c2_sweep": c2_sweep, "c1_latency": c1_latency,
                 "mean_psnr_db": {str(r): float(np.mean(ps[k])) for k, r in enumerate(R_SET)}}
         print(json.dumps(line), flush=True)

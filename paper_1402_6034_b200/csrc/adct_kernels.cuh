@@ -549,6 +549,12 @@ constexpr int compress_minb(int R) {
   return compress_resid_r(R) ? ADCT_MINB_RESID : (R == 1 ? 6 : 4);
 }
 
+#ifndef ADCT_QUANT_RING_R
+#define ADCT_QUANT_RING_R 1
+#endif
+#ifndef ADCT_ZONAL_RING_R
+#define ADCT_ZONAL_RING_R 0
+#endif
 template <int R, int MODE, int RECON, int ST = compress_stages(R),
           int MINB = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_minb(R)
                      : ((MODE == MODE_QUANT && RECON == REC_NONE && R == 64) ? ADCT_MINB_QRES : ADCT_MINB_RT),
@@ -572,8 +578,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
   const float fxs = (float)(kSseScale * p.fx_scale);  // kernel units -> fixed-point pixel^2 units
   int cur = -1;
   long long acc = 0;
-  tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
-                      [&](const uint8_t* tile, int img, int ty, int tx) {
+  auto tile_body = [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {  // warp-uniform: flush the finished image's partial SSE
       const long long v = warp_sum_ll(acc);
       if (lane == 0 && cur >= 0) fx_flush(p.sse + cur, v);
@@ -599,7 +604,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
       e2 = compress_inv<R, MODE, RECON, F16, GRP, false, MIRB>(Y, tile, lane, p, img, ty, tx);
     }
     acc += fx_lane(e2, fxs);
-  });
+  };
+  // C4's quantiser body is ~1300 instructions: one copy of it (run-time ring stage) so the warps
+  // do not stall on instruction fetch; the smaller zonal bodies keep the stage-unrolled ring
+  if constexpr ((MODE == MODE_QUANT && RECON == REC_NONE && R == 64 && ADCT_QUANT_RING_R) ||
+                (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT && ADCT_ZONAL_RING_R))
+    tma_ring_loop_r<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane, tile_body);
+  else
+    tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane, tile_body);
   const long long v = warp_sum_ll(acc);
   if (lane == 0 && cur >= 0) fx_flush(p.sse + cur, v);
 }
@@ -1556,7 +1568,8 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INC_MINB)
       cur = img;
     }
     uint32_t Y[8][8];
-    compress_fwd<36, MODE_ZONAL>(tile, lane, Y);
+    constexpr bool MIRB = ADCT_MIRB;  // block B column-mirrored (pack_rows_mirb): SSE only, errors mirrored
+    compress_fwd<36, MODE_ZONAL, MIRB>(tile, lane, Y);
     float2 V[64];
     static_for<64>([&](auto KLc) {
       constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
@@ -1577,8 +1590,9 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INC_MINB)
         constexpr int N = decltype(Nc)::value;
         // 576 (1024 + x) - 589824 = 576 x through the mixed-precision FMA (exact)
         constexpr uint32_t sel = ((N >> 1) & 1) ? 0x4342u : 0x4140u;
+        constexpr uint32_t selb = MIRB ? (((N >> 1) & 1) ? 0x4041u : 0x4243u) : sel;
         const uint32_t ha = __byte_perm(N < 4 ? wa.x : wa.y, p.h16magic, sel);
-        const uint32_t hb = __byte_perm(N < 4 ? wb.x : wb.y, p.h16magic, sel);
+        const uint32_t hb = __byte_perm((N < 4) != MIRB ? wb.x : wb.y, p.h16magic, selb);
         e[N] = make_float2(fhfma576<(N & 1) != 0, true>(ha, -DC_BIAS16), fhfma576<(N & 1) != 0, true>(hb, -DC_BIAS16));
       });
       static_for<NB>([&](auto Bc) {

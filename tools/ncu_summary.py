@@ -52,7 +52,7 @@ if tj:
     comp = [v["dram_bytes_per_px"] for k, v in per.items() if "k_compress" in k]
     with open(tj, "w") as f:
         json.dump({"source": f"ncu --set full, {int(tiles)} tiles of 4 KiB per launch "
-                             f"(summary: profiles/r01_ncu_full_summary_session4.txt)",
+                             f"(summary: profiles/r02_ncu_full_summary.txt)",
                    "dram_bytes_per_px": sum(comp) / max(1, len(comp)), "per_kernel": per}, f, indent=1)
 
 src = run("--page", "source", "--csv", "--print-source", "sass").split("\n")

@@ -44,7 +44,7 @@ import concurrent.futures as cf  # noqa: E402
 with cf.ThreadPoolExecutor(len(rs)) as ex:
     outs = list(ex.map(one, rs))
 for r, (obj, regs) in zip(rs, outs):
-    res = SR.analyse([obj], {r})
+    res = SR.analyse([obj], {r}, mode=1 if a.quant else 0)
     n, c = res[r]
     cnt, cyc = SR.breakdown(obj, r)
     top = ", ".join(f"{k} {cnt[k]}/{cyc[k]}" for k, _ in cyc.most_common(7))

@@ -42,14 +42,15 @@ def instr_cost(op, args):
     return max(1, len(even), len(odd))
 
 
-def analyse(objs, only=None):
+def analyse(objs, only=None, mode=0, recon=0):
+    """{r: (instructions, read cycles)} of the k_compress<r, mode, recon, ...> bodies in objs."""
     res = {}
     for o in objs:
         sass = subprocess.run(["cuobjdump", "-sass", o], capture_output=True, text=True).stdout
         for blk in sass.split("Function : ")[1:]:
             name = blk.split("\n")[0]
-            m = re.search(r"k_compressILi(\d+)E", name)
-            if not m:
+            m = re.search(r"k_compressILi(\d+)ELi(\d+)ELi(\d+)E", name)
+            if not m or int(m.group(2)) != mode or int(m.group(3)) != recon:
                 continue
             r = int(m.group(1))
             if only and r not in only:
@@ -64,12 +65,29 @@ def analyse(objs, only=None):
             waits = [i for i, op in enumerate(names) if op == "SYNCS" and i > body[0]]
             seg = ops[body[0]:waits[0]] if waits else ops[body[0]:body[-1]]
             cyc = sum(instr_cost(op, a) for op, a in seg)
-            res[r] = (len(seg), cyc)
+            if r not in res or cyc < res[r][1]:  # several instantiations (e.g. QLO): the lightest
+                res[r] = (len(seg), cyc)
     return res
+
+
+def write_json(path):
+    """Per-r read cycles of the built zonal kernels and of C4's quantiser kernel (bench.py reads it)."""
+    import json
+    zon = analyse(sorted(glob.glob(os.path.join(ROOT, "build/obj/zonal_part*.o"))))
+    qua = analyse([os.path.join(ROOT, "build/obj/adct_api.o")], {64}, mode=1)
+    out = {"model": "register-file read cycles per 16 x 256 tile per SMSP (tools/sass_regread.py): per instruction "
+                    "max(1, #even-bank, #odd-bank distinct non-reused register operands); peak = 1 per clock per SMSP",
+           "zonal": {str(r): {"instr": n, "read_cycles": c} for r, (n, c) in sorted(zon.items())},
+           "quant64": {"instr": qua[64][0], "read_cycles": qua[64][1]} if 64 in qua else None}
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
 
 
 if __name__ == "__main__":
     args = sys.argv[1:]
+    if "--json" in args:
+        write_json(args[args.index("--json") + 1])
+        sys.exit(0)
     only = None
     if "--r" in args:
         i = args.index("--r")
