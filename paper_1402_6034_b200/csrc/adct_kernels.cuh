@@ -545,8 +545,11 @@ constexpr bool compress_grouped(int R) { return ADCT_GROUPED || (R >= 11 && R < 
 #ifndef ADCT_MINB_RESID
 #define ADCT_MINB_RESID 4
 #endif
+#ifndef ADCT_MINB_R3
+#define ADCT_MINB_R3 3  // r = 2, 3 (3-stage ring): 4 CTAs/SM spilled (LDL/STL); 3 CTAs: r = 3 0.91 -> 0.96 of HBM (profiles/r02_variants_r3_minb.txt)
+#endif
 constexpr int compress_minb(int R) {
-  return compress_resid_r(R) ? ADCT_MINB_RESID : (R == 1 ? 6 : 4);
+  return compress_resid_r(R) ? ADCT_MINB_RESID : (R == 1 ? 6 : (R == 2 || R == 3) ? ADCT_MINB_R3 : 4);
 }
 
 #ifndef ADCT_QUANT_RING_R
@@ -554,6 +557,10 @@ constexpr int compress_minb(int R) {
 #endif
 #ifndef ADCT_ZONAL_RING_R
 #define ADCT_ZONAL_RING_R 0
+#endif
+// run-time-stage ring (one body copy) for the other large-body kernels (A/B: tools/time_variants.py)
+#ifndef ADCT_BIG_RING_R
+#define ADCT_BIG_RING_R 1
 #endif
 template <int R, int MODE, int RECON, int ST = compress_stages(R),
           int MINB = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_minb(R)
@@ -608,7 +615,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
   // C4's quantiser body is ~1300 instructions: one copy of it (run-time ring stage) so the warps
   // do not stall on instruction fetch; the smaller zonal bodies keep the stage-unrolled ring
   if constexpr ((MODE == MODE_QUANT && RECON == REC_NONE && R == 64 && ADCT_QUANT_RING_R) ||
-                (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT && ADCT_ZONAL_RING_R))
+                (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT && ADCT_ZONAL_RING_R) ||
+                (R == RT && ADCT_BIG_RING_R))
     tma_ring_loop_r<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane, tile_body);
   else
     tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane, tile_body);
@@ -666,7 +674,7 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_MINB_RT)
   const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
   int cur = -1;
   unsigned long long acc = 0ull;
-  tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
+  tma_ring_loop<(bool)ADCT_BIG_RING_R, ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
                       [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {  // warp-uniform: flush the finished image's partial sum
       const unsigned long long v = warp_sum_u64(acc);
@@ -1092,7 +1100,7 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_MINB_RT)
   const float fxs = (float)(kSseScale * p.fx_scale);
   int cur = -1;
   long long acc = 0;
-  tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
+  tma_ring_loop<(bool)ADCT_BIG_RING_R, ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
                       [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {  // warp-uniform: flush the finished image's partial SSE
       const long long v = warp_sum_ll(acc);
@@ -1214,7 +1222,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3)
   const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
   int cur = -1;
   long long acc = 0;
-  tma_ring_loop_u<STAGES>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
+  tma_ring_loop<(bool)ADCT_BIG_RING_R, STAGES>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {
       const long long v = warp_sum_ll(acc);
       if (lane == 0 && cur >= 0) fx_flush(p.sse + cur, v);
@@ -1294,7 +1302,7 @@ __global__ void __launch_bounds__(WARPS * 32, DIAG_MINB)
       E[s] = 0;
     }
   };
-  tma_ring_loop_u<DIAG_ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
+  tma_ring_loop<(bool)ADCT_BIG_RING_R, DIAG_ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane, [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {
       flush(cur);
       cur = img;
@@ -1487,7 +1495,7 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_MULTI_MINB)
       acc[k] = 0;
     }
   };
-  tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
+  tma_ring_loop<(bool)ADCT_BIG_RING_R, ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
                       [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {  // warp-uniform
       flush();
@@ -1561,7 +1569,7 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INC_MINB)
       dacc[b] = 0;
     }
   };
-  tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
+  tma_ring_loop<(bool)ADCT_BIG_RING_R, ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
                       [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {  // warp-uniform
       flush();
@@ -1679,7 +1687,7 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_MINB_RT)
   const float fxs = (float)(p.fx_scale / 4096.0);  // e = 64 (x - x^)
   int cur = -1;
   long long acc = 0;
-  tma_ring_loop_u<ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
+  tma_ring_loop<(bool)ADCT_BIG_RING_R, ST>(&tmap, plan, (int)blockIdx.x * WARPS + warp, ring, bars, lane,
                       [&](const uint8_t* tile, int img, int ty, int tx) {
     if (img != cur) {
       const long long v = warp_sum_ll(acc);

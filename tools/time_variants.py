@@ -11,6 +11,10 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
+from paper_1402_6034_b200 import _lib  # noqa: E402
+if os.environ.get("ADCT_LIB"):  # time another build (tools/build_variant.py)
+    _lib.LIB_PATH = os.environ["ADCT_LIB"]
+    os.environ["ADCT_LENIENT_LOAD"] = "1"
 import paper_1402_6034_b200 as A  # noqa: E402
 from synth import images as S  # noqa: E402
 
@@ -59,6 +63,13 @@ def main():
     add("zonal r=10 exact u64 SSE (adct_compress_sse576)", best_ms(lambda: A.compress_sse576(x, 10, sse576=s576)), 1)
     add("quant q=16 SSE only", best_ms(lambda: A.compress_psnr(x, 64, q=16.0, sse=sse)), 1)
     add("quant q=16 + u8 recon", best_ms(lambda: A.compress_psnr(x, 64, q=16.0, sse=sse, recon="u8", recon_out=rec_u)), 2)
+    add("quant q=16 r=36 SSE only (runtime mask)", best_ms(lambda: A.compress_psnr(x, 36, q=16.0, sse=sse)), 1)
+    add("quant q=16 + f32 recon", best_ms(lambda: A.compress_psnr(x, 64, q=16.0, sse=sse, recon="f32", recon_out=rec_f)), 5)
+    if hasattr(A.load(), "adct_compress_psnr_sdct"):
+        add("SDCT integer fast path r=10", best_ms(lambda: A.compress_psnr_sdct(x, 10, sse=sse)), 1)
+    add("dense exact DCT r=10", best_ms(lambda: A.compress_psnr_dense(x, 10, "dct", sse=sse)), 1)
+    msm = best_ms(lambda: A.compress_psnr_multi(x, (1, 3, 6, 10, 15, 21, 28, 36)))
+    rows.append(("fused multi-r sweep (8 r, Gpix-passes/s)", 8 * px / (msm * 1e-3) / 1e9, px / (msm * 1e-3) / 1e9 / pk, msm))
     add("forward int16 (r=64)", best_ms(lambda: A.forward(x, out=coef)), 3)
     add("inverse int16 -> f32 (r=64)", best_ms(lambda: A.inverse(coef, r=64, out="f32", dst=rec_f)), 6)
     del x, rec_f, rec_u, coef
@@ -67,6 +78,7 @@ def main():
     ssev = torch.empty(8, dtype=torch.float64, device="cuda")
     ms = best_ms(lambda: A.compress_psnr(v, 64, q=16.0, sse=ssev))
     rows.append(("C4 frames 8 x 4320x7680 quant q=16 SSE only", pxv / (ms * 1e-3) / 1e9, pxv / (ms * 1e-3) / 1e9 / pk, ms))
+    print(f"# {os.environ.get('ADCT_LIB', 'default build')}")
     print(f"# variants on one B200 (32 x 4096^2 C5-kind images unless noted); HBM fraction of {pk:.0f} GB/s "
           f"at the algorithmic bytes/px (1 read + output)")
     print(f"{'variant':48s} {'Gpix/s':>9s} {'HBM frac':>9s} {'ms':>9s}")
