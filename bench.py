@@ -433,7 +433,11 @@ def main():
     ems = max_over_ranks(e0.elapsed_time(e1), dev)
     e2e = {"value": world * ne * H * W * len(R_SET) / (ems / e_steps * 1e-3) / 1e9, "unit": UNIT,
            "h2d_bytes_per_step": ne * H * W, "d2h_bytes_per_step": len(R_SET) * ne * 8,
-           "images_per_rank": ne, "api": "adct_compress_psnr_host (caller copy stream, fused multi-r kernel)"}
+           "images_per_rank": ne, "api": "adct_compress_psnr_host (caller copy stream, fused multi-r kernel)",
+           # the e2e step is bound by the host->device copy: its achieved PCIe rate (per rank)
+           "h2d_gb_s_per_rank": ne * H * W / (ems / e_steps * 1e-3) / 1e9,
+           "h2d_note": "PCIe Gen5 x16: 64 GB/s nominal per direction; the device work per copied byte "
+                       "(8 r-passes) runs ~20x faster than the copy"}
 
     # ---- secondary (N = 1): forward-only C3 (8192 x 512^2 uniform, int16 out), 3 B/px
     fwd_only = None

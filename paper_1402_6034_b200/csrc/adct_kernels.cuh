@@ -549,7 +549,8 @@ constexpr bool compress_grouped(int R) { return ADCT_GROUPED || (R >= 11 && R < 
 #define ADCT_MINB_R3 3  // r = 2, 3 (3-stage ring): 4 CTAs/SM spilled (LDL/STL); 3 CTAs: r = 3 0.91 -> 0.96 of HBM (profiles/r02_variants_r3_minb.txt)
 #endif
 constexpr int compress_minb(int R) {
-  return compress_resid_r(R) ? ADCT_MINB_RESID : (R == 1 ? 6 : (R == 2 || R == 3) ? ADCT_MINB_R3 : 4);
+  // r = 64 (lossless, all 64 coefficients through the direct form): 2 CTAs/SM, no spills (4 spilled 824 B)
+  return compress_resid_r(R) ? ADCT_MINB_RESID : (R == 1 ? 6 : (R == 2 || R == 3) ? ADCT_MINB_R3 : R == 64 ? 2 : 4);
 }
 
 #ifndef ADCT_QUANT_RING_R
