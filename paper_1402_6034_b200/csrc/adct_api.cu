@@ -144,7 +144,16 @@ float quant_recip(float q, int dd) {
   return c;
 }
 
+// the uniform multiplicand pairs of the one-instruction butterflies (adct_device.cuh inv8s / inv8ws)
+void fill_bfly_pairs(Tables& t) {
+  t.pm1 = make_float2(1.f, -1.f);
+  t.pmr = make_float2(-1.f, 1.f);
+  t.ps2 = make_float2(QW_S2, -QW_S2);
+  t.pro = make_float2(QW_RO, -QW_RO);
+}
+
 void fill_zonal_tables(Tables& t, int r) {
+  fill_bfly_pairs(t);
   for (int k = 0; k < 8; ++k)
     for (int l = 0; l < 8; ++l) {
       t.wc[wclass(k, l)] = (float)wval(k, l);
@@ -160,6 +169,7 @@ void fill_zonal_tables(Tables& t, int r) {
 }
 
 void fill_quant_tables(Tables& t, int r, float q) {
+  fill_bfly_pairs(t);
   for (int k = 0; k < 8; ++k)
     for (int l = 0; l < 8; ++l) {
       const bool keep = zz_host(k, l) < r;

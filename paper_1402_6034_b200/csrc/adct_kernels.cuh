@@ -36,6 +36,10 @@ struct Tables {
   float sq[8];   // QUANT residual form: 1 / (q sqrt dd) per weight class as hi + lo fp32 pair
   float sql[8];
   float qscale;  // QUANT residual form: SSE = (q / 8)^2 * sum of the weighted inverse's squares
+  float2 pm1;    // (1, -1): the uniform multiplicand pair of the one-instruction butterflies (inv8s)
+  float2 pmr;    // (-1, 1): the swapped butterfly (sum in .y), inv8p's register-bank planning
+  float2 ps2;    // (sqrt 2, -sqrt 2), (2 / sqrt 3, -2 / sqrt 3): the quantiser's weighted butterflies
+  float2 pro;
 };
 
 // Deterministic per-image sums ("identical to sequential execution"; SURVEY §7 hard part 5):
@@ -283,7 +287,73 @@ template <int N> __device__ __forceinline__ float2 err_fh(uint32_t ha, uint32_t 
   return err_fh<N, true>(ha, hb, r.v);
 }
 
-template <int R, int MODE, int RECON, int F16 = 0, bool GROUPED = false, bool STAGE = false, bool MIRB = false>
+// Scalar-per-block inverse (inverse2d_s, adct_device.cuh) -> the (block A, block B) view the error
+// callbacks use: output n of both blocks as one typed value (no register pair is formed for the
+// scalar consumers, FHFMA / FFMA).
+// Inverse flavour per kernel (template parameter SM): 0 = f32x2 FADD2 over the (A, B) block pair,
+// 1 = per-block scalar one-instruction butterflies (inv8s), 2 = the same with a register-bank plan
+// (inv8p).  Measured on B200 (profiles/r02_variants_inverse_flavour.txt, 1024 C5 images): SM = 1 wins
+// for the direct form at small r (r = 6: 0.75 -> 0.85 of HBM, r = 10: 0.63 -> 0.69) and for the
+// residual form (r = 28: 0.57 -> 0.60, r = 36: 0.61 -> 0.66); the grouped mid-r kernels (11 <= r < 24)
+// and C4's quantiser keep SM = 0; the bank plan (SM = 2) did not pay (ptxas re-assigns registers).
+#ifndef ADCT_SINV
+#define ADCT_SINV -1  // -1: the measured per-kernel choice (sinv_mode); 0 / 1 / 2 force one flavour
+#endif
+template <bool N> __device__ __forceinline__ FV<N> join_ab(SV<N> a, SV<N> b) { return {make_float2(a.v, b.v)}; }
+__device__ __forceinline__ Z0 join_ab(Z0, Z0) { return {}; }
+template <class RA, class RB> __device__ __forceinline__ auto join_rows(const RA& ra, const RB& rb) {
+  using cuda::std::get;
+  return cuda::std::make_tuple(join_ab(get<0>(ra), get<0>(rb)), join_ab(get<1>(ra), get<1>(rb)),
+                               join_ab(get<2>(ra), get<2>(rb)), join_ab(get<3>(ra), get<3>(rb)),
+                               join_ab(get<4>(ra), get<4>(rb)), join_ab(get<5>(ra), get<5>(rb)),
+                               join_ab(get<6>(ra), get<6>(rb)), join_ab(get<7>(ra), get<7>(rb)));
+}
+// acc += (a, b)^2 for outputs n, 7 - n of ONE block (they leave one butterfly as a register pair)
+__device__ __forceinline__ float2 sq2(Z0, Z0, float2 acc) { return acc; }
+template <bool NA> __device__ __forceinline__ float2 sq2(SV<NA> a, Z0, float2 acc) {
+  return make_float2(fmaf(a.v, a.v, acc.x), acc.y);
+}
+template <bool NB> __device__ __forceinline__ float2 sq2(Z0, SV<NB> b, float2 acc) {
+  return make_float2(acc.x, fmaf(b.v, b.v, acc.y));
+}
+template <bool NA, bool NB> __device__ __forceinline__ float2 sq2(SV<NA> a, SV<NB> b, float2 acc) {
+  const float2 v = make_float2(a.v, b.v);
+  return f2fma(v, v, acc);
+}
+
+// block BLK's biased float 2^23 + 2^15 + Y of a packed coefficient (the halves of biased_pair)
+template <int BLK> __device__ __forceinline__ float bpf(uint32_t Pb) {
+  return __uint_as_float(__byte_perm(Pb, 0x4B000000u, BLK ? 0x7632 : 0x7610));
+}
+// W . Y of the kept set KS (compile-time mask) into per-block scalar planes, the column partners
+// (0,4), (6,2), (1,3), (7,5) converted as one register pair each (inv8p's input parity pattern);
+// partners share the weight class.  dc adds a constant to coefficient (0, 0) (the f16 route's bias).
+template <int KS>
+__device__ __forceinline__ void convert_planned(const uint32_t (&Y)[8][8], const CompressParams& p, float dc,
+                                                float (&VS)[2][64]) {
+  static_for<64>([&](auto KLc) {
+    constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8, k2 = pair_partner(k);
+    constexpr int c = wclass(k, l);
+    static_assert(wclass(k, l) == wclass(k2, l), "partners share the weight class");
+    if constexpr (kept(KS, k, l) && pair_lead(k) && kept(KS, k2, l)) {
+      const float cc = p.tab.cc[c];
+      const float c0 = kl == 0 ? cc + dc : cc;
+      static_for<2>([&](auto Bc) {
+        constexpr int B = decltype(Bc)::value;
+        const float2 v = f2fma(make_float2(bpf<B>(Y[k][l]), bpf<B>(Y[k2][l])), f2(p.tab.wc[c]), make_float2(c0, cc));
+        VS[B][k * 8 + l] = v.x;
+        VS[B][k2 * 8 + l] = v.y;
+      });
+    } else if constexpr (kept(KS, k, l) && !kept(KS, k2, l)) {  // lone member: a scalar FFMA
+      const float cc = kl == 0 ? p.tab.cc[c] + dc : p.tab.cc[c];
+      VS[0][kl] = fmaf(bpf<0>(Y[k][l]), p.tab.wc[c], cc);
+      VS[1][kl] = fmaf(bpf<1>(Y[k][l]), p.tab.wc[c], cc);
+    }
+  });
+}
+
+template <int R, int MODE, int RECON, int F16 = 0, bool GROUPED = false, bool STAGE = false, bool MIRB = false,
+          int SM = 0>
 __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const uint8_t* tile, int lane,
                                                const CompressParams& p, int img, int ty, int tx,
                                                uint8_t* sbuf = nullptr) {
@@ -356,8 +426,21 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
     else if constexpr (RECON != REC_NONE)
       store_recon_row<RECON, (MODE == MODE_ZONAL), (MODE == MODE_ZONAL ? U8_FAST576 : U8_SAFEX)>(rbase, p.recon_pitch, p.h, p.w, ty * TILE_H + I, col, xr);
   };
-  if constexpr (GROUPED) inverse2d_grouped<RF>(V, err_row);
-  else inverse2d<RF>(V, err_row);
+  if constexpr (SM == 2 && MODE == MODE_ZONAL && RF < RT && !GROUPED) {
+    // bank-planned scalar inverse (inv8p) on per-block planes converted as register pairs
+    float VS[2][64], UHS[2][8][8];
+    convert_planned<RF>(Y, p, F16 > 0 ? DC_BIAS16 : 0.f, VS);
+    auto err_row_s = [&](auto Ic, const auto& ra, const auto& rb) { err_row(Ic, join_rows(ra, rb)); };
+    inverse2d_p<RF>(VS, UHS, p.tab.pm1, p.tab.pmr, err_row_s);
+  } else if constexpr (SM != 0) {
+    auto err_row_s = [&](auto Ic, const auto& ra, const auto& rb) { err_row(Ic, join_rows(ra, rb)); };
+    float2 UH[8][8];  // unused (no injected columns in the direct form)
+    if constexpr (GROUPED) inverse2d_s_grouped<RF>(V, p.tab.pm1, err_row_s);
+    else inverse2d_s<RF>(V, UH, p.tab.pm1, err_row_s);
+  } else {
+    if constexpr (GROUPED) inverse2d_grouped<RF>(V, err_row);
+    else inverse2d<RF>(V, err_row);
+  }
   const float2 s01 = f2add(acc[0], acc[1]), s23 = f2add(acc[2], acc[3]);
   const float2 s45 = f2add(acc[4], acc[5]), s67 = f2add(acc[6], acc[7]);
   return f2add(f2add(s01, s23), f2add(s45, s67));
@@ -370,7 +453,7 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
 // coefficients the mask discards.  Every node is an integer below 2^24 (tools/exactness_bounds.py),
 // so this equals the direct form bit for bit; it needs no pixel re-read and no 576 x, and for
 // large r the discarded set is the smaller one.  Returns the lane's sum of e^2 (576 units).
-template <int R, bool GROUPED = false>
+template <int R, bool GROUPED = false, int SM = 0>
 __device__ __forceinline__ float2 compress_resid(const uint32_t (&Y)[8][8], const CompressParams& p) {
   constexpr int RM = RESID + R;
   float2 V[64];
@@ -391,8 +474,27 @@ __device__ __forceinline__ float2 compress_resid(const uint32_t (&Y)[8][8], cons
       acc[N] = sqacc(get<N>(row), acc[N]);
     });
   };
-  if constexpr (GROUPED) inverse2d_grouped<RM>(V, sq_row);
-  else inverse2d<RM>(V, sq_row);
+  // per block: outputs n and 7 - n leave one butterfly as a register pair -> one FFMA2 per pair
+  auto sq_row_s = [&](auto Ic, const auto& ra, const auto& rb) {
+    using cuda::std::get;
+    static_for<4>([&](auto Nc) {
+      constexpr int N = decltype(Nc)::value;
+      acc[N] = sq2(get<N>(ra), get<7 - N>(ra), acc[N]);
+      acc[4 + N] = sq2(get<N>(rb), get<7 - N>(rb), acc[4 + N]);
+    });
+  };
+  if constexpr (SM == 2 && !GROUPED) {
+    float VS[2][64], UHS[2][8][8];
+    convert_planned<RM>(Y, p, 0.f, VS);
+    inverse2d_p<RM>(VS, UHS, p.tab.pm1, p.tab.pmr, sq_row_s);
+  } else if constexpr (SM != 0) {
+    float2 UH[8][8];
+    if constexpr (GROUPED) inverse2d_s_grouped<RM>(V, p.tab.pm1, sq_row_s);
+    else inverse2d_s<RM>(V, UH, p.tab.pm1, sq_row_s);
+  } else {
+    if constexpr (GROUPED) inverse2d_grouped<RM>(V, sq_row);
+    else inverse2d<RM>(V, sq_row);
+  }
   const float2 s01 = f2add(acc[0], acc[1]), s23 = f2add(acc[2], acc[3]);
   const float2 s45 = f2add(acc[4], acc[5]), s67 = f2add(acc[6], acc[7]);
   return f2add(f2add(s01, s23), f2add(s45, s67));
@@ -404,7 +506,7 @@ __device__ __forceinline__ float2 compress_resid(const uint32_t (&Y)[8][8], cons
 #ifndef ADCT_RESID_HC
 #define ADCT_RESID_HC 1
 #endif
-template <int R>
+template <int R, int SM = 0>
 __device__ __forceinline__ float2 compress_resid_hc(const uint32_t (&Y)[8][8], const uint32_t (&H)[8][8],
                                                     const CompressParams& p) {
   constexpr int RM = RESID + R, HC = hcol_mask(R);
@@ -429,14 +531,47 @@ __device__ __forceinline__ float2 compress_resid_hc(const uint32_t (&Y)[8][8], c
   float2 acc[8];
 #pragma unroll
   for (int n = 0; n < 8; ++n) acc[n] = f2(0.f);
-  auto sq_row = [&](auto Ic, auto row) {
-    using cuda::std::get;
-    static_for<8>([&](auto Nc) {
-      constexpr int N = decltype(Nc)::value;
-      acc[N] = sqacc(get<N>(row), acc[N]);
-    });
-  };
-  inverse2d_hc<RM, HC>(V, UH, sq_row);
+  if constexpr (SM != 0) {
+    auto sq_row_s = [&](auto Ic, const auto& ra, const auto& rb) {
+      using cuda::std::get;
+      static_for<4>([&](auto Nc) {
+        constexpr int N = decltype(Nc)::value;
+        acc[N] = sq2(get<N>(ra), get<7 - N>(ra), acc[N]);
+        acc[4 + N] = sq2(get<N>(rb), get<7 - N>(rb), acc[4 + N]);
+      });
+    };
+    if constexpr (SM == 2) {
+      float VS[2][64], UHS[2][8][8];
+      convert_planned<RM & 0 ? 0 : (RM)>(Y, p, 0.f, VS);  // (columns in HC are never read)
+      static_for<8>([&](auto Lc) {
+        constexpr int L = decltype(Lc)::value;
+        if constexpr ((HC >> L) & 1) {
+          constexpr float wl = (float)(576 / dval(L));
+#pragma unroll
+          for (int i = 0; i < 4; ++i)  // rows (i, 7 - i) as one register pair per block (inv8p's row pattern)
+            static_for<2>([&](auto Bc) {
+              constexpr int B = decltype(Bc)::value;
+              const float2 v = f2fma(make_float2(bpf<B>(H[i][L] + BIAS2), bpf<B>(H[7 - i][L] + BIAS2)), f2(wl),
+                                     f2(-KF * wl));
+              UHS[B][L][i] = v.x;
+              UHS[B][L][7 - i] = v.y;
+            });
+        }
+      });
+      inverse2d_p<RM, HC>(VS, UHS, p.tab.pm1, p.tab.pmr, sq_row_s);
+    } else {
+      inverse2d_s<RM, HC>(V, UH, p.tab.pm1, sq_row_s);
+    }
+  } else {
+    auto sq_row = [&](auto Ic, auto row) {
+      using cuda::std::get;
+      static_for<8>([&](auto Nc) {
+        constexpr int N = decltype(Nc)::value;
+        acc[N] = sqacc(get<N>(row), acc[N]);
+      });
+    };
+    inverse2d_hc<RM, HC>(V, UH, sq_row);
+  }
   const float2 s01 = f2add(acc[0], acc[1]), s23 = f2add(acc[2], acc[3]);
   const float2 s45 = f2add(acc[4], acc[5]), s67 = f2add(acc[6], acc[7]);
   return f2add(f2add(s01, s23), f2add(s45, s67));
@@ -473,7 +608,25 @@ __device__ __forceinline__ void inv8w(const float2 (&v)[8], float2 (&o)[8]) {
 // of two) stays exact, so P18's constant frames are still bit-exact; one FFMA2 (two register-read
 // cycles) less per coefficient pair.  The host picks LO for q < 4, where |Y / (q sqrt dd)| (up to
 // 16320 / (4 q)) makes that rounding visible at the SSE bar (adct_api.cu).
-template <bool LO>
+// the same weighted graph per block on scalars with one-instruction butterflies: (x + w y, x - w y)
+// with the uniform pairs (1, -1), (sqrt 2, -sqrt 2), (2 / sqrt 3, -2 / sqrt 3) — the same single-rounded
+// fused products as inv8w
+__device__ __forceinline__ void inv8ws(const float (&v)[8], float (&o)[8], float2 pm, float2 ps, float2 pr) {
+  const float2 pq = ffma2_bfly(v[0], v[4], pm);      // pp, qq
+  const float2 a03 = ffma2_bfly(pq.x, v[2], ps);     // pp +- s2 v2
+  const float2 a21 = ffma2_bfly(pq.y, v[6], ps);     // qq +- s2 v6: (a2, a1)
+  const float2 s13 = ffma2_bfly(v[1], v[3], pm);     // v1 +- v3
+  const float2 s57 = ffma2_bfly(v[5], v[7], pm);     // v5 +- v7
+  const float b0 = s13.x + v[5], b1 = v[1] - s57.x, b2 = s13.y + v[7], b3 = s57.y - v[3];
+  const float2 o07 = ffma2_bfly(a03.x, b0, pr);
+  const float2 o16 = ffma2_bfly(a21.y, b1, pr);
+  const float2 o25 = ffma2_bfly(a21.x, b2, pr);
+  const float2 o34 = ffma2_bfly(a03.y, b3, pr);
+  o[0] = o07.x; o[7] = o07.y; o[1] = o16.x; o[6] = o16.y;
+  o[2] = o25.x; o[5] = o25.y; o[3] = o34.x; o[4] = o34.y;
+}
+
+template <bool LO, int SM = 0>
 __device__ __forceinline__ float2 compress_quant_resid(const uint32_t (&Y)[8][8], const CompressParams& p) {
   float2 U[8][8];  // column pass outputs [row][col]
   static_for<8>([&](auto Lc) {
@@ -492,19 +645,48 @@ __device__ __forceinline__ float2 compress_quant_resid(const uint32_t (&Y)[8][8]
       else
         v[K] = f2fma(y, f2(p.tab.sq[c]), make_float2(-k.x, -k.y));
     });
-    inv8w(v, o);
+    if constexpr (SM != 0) {
+      float va[8], vb[8], oa[8], ob[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) U[i][L] = o[i];
+      for (int k = 0; k < 8; ++k) {
+        va[k] = v[k].x;
+        vb[k] = v[k].y;
+      }
+      inv8ws(va, oa, p.tab.pm1, p.tab.ps2, p.tab.pro);
+      inv8ws(vb, ob, p.tab.pm1, p.tab.ps2, p.tab.pro);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) U[i][L] = make_float2(oa[i], ob[i]);
+    } else {
+      inv8w(v, o);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) U[i][L] = o[i];
+    }
   });
   float2 acc[8];
 #pragma unroll
   for (int n = 0; n < 8; ++n) acc[n] = f2(0.f);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    float2 o[8];
-    inv8w(U[i], o);
+    if constexpr (SM != 0) {
+      float ua[8], ub[8], oa[8], ob[8];
 #pragma unroll
-    for (int n = 0; n < 8; ++n) acc[n] = f2fma(o[n], o[n], acc[n]);
+      for (int l = 0; l < 8; ++l) {
+        ua[l] = U[i][l].x;
+        ub[l] = U[i][l].y;
+      }
+      inv8ws(ua, oa, p.tab.pm1, p.tab.ps2, p.tab.pro);
+      inv8ws(ub, ob, p.tab.pm1, p.tab.ps2, p.tab.pro);
+#pragma unroll
+      for (int n = 0; n < 4; ++n) {  // outputs n, 7 - n of one block leave one butterfly as a pair
+        acc[n] = f2fma(make_float2(oa[n], oa[7 - n]), make_float2(oa[n], oa[7 - n]), acc[n]);
+        acc[4 + n] = f2fma(make_float2(ob[n], ob[7 - n]), make_float2(ob[n], ob[7 - n]), acc[4 + n]);
+      }
+    } else {
+      float2 o[8];
+      inv8w(U[i], o);
+#pragma unroll
+      for (int n = 0; n < 8; ++n) acc[n] = f2fma(o[n], o[n], acc[n]);
+    }
   }
   const float2 s01 = f2add(acc[0], acc[1]), s23 = f2add(acc[2], acc[3]);
   const float2 s45 = f2add(acc[4], acc[5]), s67 = f2add(acc[6], acc[7]);
@@ -533,7 +715,10 @@ constexpr int compress_f16_rows(int R) { return R == 1 ? 6 : 8; }
 #ifndef ADCT_GROUPED
 #define ADCT_GROUPED 0
 #endif
-constexpr bool compress_grouped(int R) { return ADCT_GROUPED || (R >= 11 && R < ADCT_RESID_FROM); }
+#ifndef ADCT_NOGROUP
+#define ADCT_NOGROUP 0
+#endif
+constexpr bool compress_grouped(int R) { return !ADCT_NOGROUP && (ADCT_GROUPED || (R >= 11 && R < ADCT_RESID_FROM)); }
 // runtime-mask / quantiser / reconstruction kernels (all 64 coefficients live)
 #ifndef ADCT_MINB_QRES
 #define ADCT_MINB_QRES 2
@@ -563,6 +748,10 @@ constexpr int compress_minb(int R) {
 #ifndef ADCT_BIG_RING_R
 #define ADCT_BIG_RING_R 1
 #endif
+constexpr int sinv_mode(int R, int MODE, int RECON) {
+  return ADCT_SINV >= 0 ? ADCT_SINV
+         : (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT && !compress_grouped(R)) ? 1 : 0;
+}
 template <int R, int MODE, int RECON, int ST = compress_stages(R),
           int MINB = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_minb(R)
                      : ((MODE == MODE_QUANT && RECON == REC_NONE && R == 64) ? ADCT_MINB_QRES : ADCT_MINB_RT),
@@ -570,7 +759,7 @@ template <int R, int MODE, int RECON, int ST = compress_stages(R),
           int F16 = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_f16_rows(R) : 0,
           bool GRP = (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT) ? compress_grouped(R) : false,
           bool MIRB = ADCT_MIRB && RECON == REC_NONE && ((MODE == MODE_ZONAL && R < RT) || (MODE == MODE_QUANT && R == 64)),
-          bool QLO = false>
+          bool QLO = false, int SM = sinv_mode(R, MODE, RECON)>
 __global__ void __launch_bounds__(WARPS * 32, MINB)
     k_compress(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CompressParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -599,17 +788,17 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
       if constexpr (ADCT_RESID_HC && hcol_mask(R) != 0 && !GRP) {
         uint32_t H[8][8];
         compress_fwd_h<RESID + R, hcol_mask(R), MIRB>(tile, lane, Y, H);
-        e2 = compress_resid_hc<R>(Y, H, p);
+        e2 = compress_resid_hc<R, SM>(Y, H, p);
       } else {
         compress_fwd<RESID + R, MODE, MIRB>(tile, lane, Y);
-        e2 = compress_resid<R, GRP>(Y, p);
+        e2 = compress_resid<R, GRP, SM>(Y, p);
       }
     } else if constexpr (MODE == MODE_QUANT && RECON == REC_NONE && R == 64) {
       compress_fwd<64, MODE, MIRB>(tile, lane, Y);
-      e2 = compress_quant_resid<QLO>(Y, p);
+      e2 = compress_quant_resid<QLO, SM>(Y, p);
     } else {
       compress_fwd<R, MODE, MIRB>(tile, lane, Y);
-      e2 = compress_inv<R, MODE, RECON, F16, GRP, false, MIRB>(Y, tile, lane, p, img, ty, tx);
+      e2 = compress_inv<R, MODE, RECON, F16, GRP, false, MIRB, SM>(Y, tile, lane, p, img, ty, tx);
     }
     acc += fx_lane(e2, fxs);
   };
@@ -1507,11 +1696,12 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_MULTI_MINB)
     static_for<RS::n>([&](auto Kc) {
       constexpr int k = decltype(Kc)::value, R = RS::r[k];
       float2 e2;
+      constexpr int SMR = sinv_mode(R, MODE_ZONAL, REC_NONE);
       if constexpr (compress_resid_r(R))
-        e2 = compress_resid<R, compress_grouped(R)>(Y, p);
+        e2 = compress_resid<R, compress_grouped(R), SMR>(Y, p);
       else
-        e2 = compress_inv<R, MODE_ZONAL, REC_NONE, compress_f16_rows(R), compress_grouped(R)>(Y, tile, lane, p,
-                                                                                              img, ty, tx);
+        e2 = compress_inv<R, MODE_ZONAL, REC_NONE, compress_f16_rows(R), compress_grouped(R), false, false, SMR>(
+            Y, tile, lane, p, img, ty, tx);
       acc[k] += fx_lane(e2, fxs);
     });
   });
@@ -1759,7 +1949,7 @@ typedef void (*CompressKernel)(CUtensorMap, CompressParams);
 // C4's quantiser kernel (compile-time r = 64, residual form) without / with the reciprocal's low part
 template <bool LO> constexpr CompressKernel quant64_kernel() {
   return &k_compress<64, MODE_QUANT, REC_NONE, compress_stages(64), ADCT_MINB_QRES, false, 0, false,
-                     (bool)ADCT_MIRB, LO>;
+                     (bool)ADCT_MIRB, LO, sinv_mode(64, MODE_QUANT, REC_NONE)>;
 }
 CompressKernel multi_kernel_c5();  // k_compress_multi<RSetC5>, instantiated in multi_r.cu
 CompressKernel sweep_inc_kernel_c5();  // k_compress_sweep_inc, instantiated in multi_r.cu
