@@ -767,6 +767,7 @@ adct_status adct_compress_psnr_sdct(const uint8_t* src, int64_t n, int64_t h, in
   p.h = (int)h;
   p.w = (int)w;
   p.sse = sse;
+  fill_bfly_pairs(p.tab);
   for (int k = 0; k < 8; ++k)
     for (int l = 0; l < 8; ++l) {
       const float m = zz_host(k, l) < r ? 1.f : 0.f;  // M_r as 0 / 1 weights (Z = Y / 8 folded in the 1/64)

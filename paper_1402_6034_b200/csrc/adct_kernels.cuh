@@ -432,6 +432,10 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
     convert_planned<RF>(Y, p, F16 > 0 ? DC_BIAS16 : 0.f, VS);
     auto err_row_s = [&](auto Ic, const auto& ra, const auto& rb) { err_row(Ic, join_rows(ra, rb)); };
     inverse2d_p<RF>(VS, UHS, p.tab.pm1, p.tab.pmr, err_row_s);
+  } else if constexpr (SM == 3) {  // f32x2 column pass, scalar-butterfly row pass
+    auto err_row_s = [&](auto Ic, const auto& ra, const auto& rb) { err_row(Ic, join_rows(ra, rb)); };
+    if constexpr (GROUPED) inverse2d_hyb_grouped<RF>(V, p.tab.pm1, err_row_s);
+    else inverse2d_hyb<RF>(V, p.tab.pm1, err_row_s);
   } else if constexpr (SM != 0) {
     auto err_row_s = [&](auto Ic, const auto& ra, const auto& rb) { err_row(Ic, join_rows(ra, rb)); };
     float2 UH[8][8];  // unused (no injected columns in the direct form)
@@ -487,6 +491,9 @@ __device__ __forceinline__ float2 compress_resid(const uint32_t (&Y)[8][8], cons
     float VS[2][64], UHS[2][8][8];
     convert_planned<RM>(Y, p, 0.f, VS);
     inverse2d_p<RM>(VS, UHS, p.tab.pm1, p.tab.pmr, sq_row_s);
+  } else if constexpr (SM == 3) {
+    if constexpr (GROUPED) inverse2d_hyb_grouped<RM>(V, p.tab.pm1, sq_row_s);
+    else inverse2d_hyb<RM>(V, p.tab.pm1, sq_row_s);
   } else if constexpr (SM != 0) {
     float2 UH[8][8];
     if constexpr (GROUPED) inverse2d_s_grouped<RM>(V, p.tab.pm1, sq_row_s);
@@ -1733,6 +1740,20 @@ template <int B, int I, int L> __device__ __forceinline__ auto band_in(const flo
   else if constexpr (c0_entry(k, I) > 0) return FV<false>{V[k * 8 + L]};
   else return FV<true>{V[k * 8 + L]};
 }
+// the same for one block (scalar, one-instruction butterflies in the row inverse)
+template <int B, int I, int L, int BLK> __device__ __forceinline__ auto band_in_s(const float2 (&V)[64]) {
+  constexpr int k = B - L;
+  if constexpr (k < 0 || k > 7) return Z0{};
+  else if constexpr (c0_entry(k, I) == 0) return Z0{};
+  else if constexpr (c0_entry(k, I) > 0) return SV<false>{BLK ? V[k * 8 + L].y : V[k * 8 + L].x};
+  else return SV<true>{BLK ? V[k * 8 + L].y : V[k * 8 + L].x};
+}
+__device__ __forceinline__ float ssub(float e, Z0) { return e; }
+__device__ __forceinline__ float ssub(float e, SV<false> r) { return e - r.v; }
+__device__ __forceinline__ float ssub(float e, SV<true> r) { return e + r.v; }
+#ifndef ADCT_SWEEP_SINV
+#define ADCT_SWEEP_SINV 1
+#endif
 
 #ifndef ADCT_INC_MINB
 #define ADCT_INC_MINB 2
@@ -1796,13 +1817,27 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INC_MINB)
       });
       static_for<NB>([&](auto Bc) {
         constexpr int B = decltype(Bc)::value;
-        auto row = inv8(band_in<B, I, 0>(V), band_in<B, I, 1>(V), band_in<B, I, 2>(V), band_in<B, I, 3>(V),
-                        band_in<B, I, 4>(V), band_in<B, I, 5>(V), band_in<B, I, 6>(V), band_in<B, I, 7>(V));
-        static_for<8>([&](auto Nc) {
-          constexpr int N = decltype(Nc)::value;
-          e[N] = rsub(e[N], cuda::std::get<N>(row));  // e_{r_B} = e_{r_{B-1}} - dR_B, exact
-          acc[B] = f2fma(e[N], e[N], acc[B]);
-        });
+        if constexpr (ADCT_SWEEP_SINV) {  // per block, one-instruction butterflies (inv8s)
+          auto ra = inv8s(band_in_s<B, I, 0, 0>(V), band_in_s<B, I, 1, 0>(V), band_in_s<B, I, 2, 0>(V),
+                          band_in_s<B, I, 3, 0>(V), band_in_s<B, I, 4, 0>(V), band_in_s<B, I, 5, 0>(V),
+                          band_in_s<B, I, 6, 0>(V), band_in_s<B, I, 7, 0>(V), p.tab.pm1);
+          auto rb = inv8s(band_in_s<B, I, 0, 1>(V), band_in_s<B, I, 1, 1>(V), band_in_s<B, I, 2, 1>(V),
+                          band_in_s<B, I, 3, 1>(V), band_in_s<B, I, 4, 1>(V), band_in_s<B, I, 5, 1>(V),
+                          band_in_s<B, I, 6, 1>(V), band_in_s<B, I, 7, 1>(V), p.tab.pm1);
+          static_for<8>([&](auto Nc) {
+            constexpr int N = decltype(Nc)::value;
+            e[N] = make_float2(ssub(e[N].x, cuda::std::get<N>(ra)), ssub(e[N].y, cuda::std::get<N>(rb)));
+            acc[B] = f2fma(e[N], e[N], acc[B]);
+          });
+        } else {
+          auto row = inv8(band_in<B, I, 0>(V), band_in<B, I, 1>(V), band_in<B, I, 2>(V), band_in<B, I, 3>(V),
+                          band_in<B, I, 4>(V), band_in<B, I, 5>(V), band_in<B, I, 6>(V), band_in<B, I, 7>(V));
+          static_for<8>([&](auto Nc) {
+            constexpr int N = decltype(Nc)::value;
+            e[N] = rsub(e[N], cuda::std::get<N>(row));  // e_{r_B} = e_{r_{B-1}} - dR_B, exact
+            acc[B] = f2fma(e[N], e[N], acc[B]);
+          });
+        }
       });
     });
 #pragma unroll
@@ -1848,6 +1883,30 @@ __device__ __forceinline__ auto inv8_sdct(X0 x0, X1 x1, X2 x2, X3 x3, X4 x4, X5 
   return cuda::std::make_tuple(add(a0, b0), add(a1, b1), add(a2, b2), add(a3, b3), sub(a3, b3), sub(a2, b2),
                                sub(a1, b1), sub(a0, b0));
 }
+// the same graph per block with one-instruction butterflies: 11 butterflies + 2 scalar adds
+template <class X0, class X1, class X2, class X3, class X4, class X5, class X6, class X7>
+__device__ __forceinline__ auto inv8s_sdct(X0 x0, X1 x1, X2 x2, X3 x3, X4 x4, X5 x5, X6 x6, X7 x7, float2 pm) {
+  using cuda::std::get;
+  const auto pq = sbfly(x0, x2, pm);            // p = x0 + x2, q = x0 - x2
+  const auto rs = sbfly(x4, x6, pm);            // r = x4 + x6, s = x4 - x6
+  const auto a01 = sbfly(get<0>(pq), get<0>(rs), pm);  // a0 = p + r, a1 = p - r
+  const auto a32 = sbfly(get<1>(pq), get<1>(rs), pm);  // a3 = q + s, a2 = q - s
+  const auto gh = sbfly(x1, x3, pm);            // g = x1 + x3, h = x1 - x3
+  const auto ij = sbfly(x5, x7, pm);            // i = x5 + x7, j = x5 - x7
+  const auto b21 = sbfly(get<1>(gh), get<0>(ij), pm);  // b2 = h + i, b1 = h - i
+  const auto b0 = add(get<0>(gh), get<0>(ij));
+  const auto b3 = add(get<1>(gh), get<1>(ij));
+  const auto o0 = sbfly(get<0>(a01), b0, pm);
+  const auto o1 = sbfly(get<1>(a01), get<1>(b21), pm);
+  const auto o2 = sbfly(get<1>(a32), get<0>(b21), pm);
+  const auto o3 = sbfly(get<0>(a32), b3, pm);
+  return cuda::std::make_tuple(get<0>(o0), get<0>(o1), get<0>(o2), get<0>(o3), get<1>(o3), get<1>(o2), get<1>(o1),
+                               get<1>(o0));
+}
+#ifndef ADCT_SDCT_SINV
+#define ADCT_SDCT_SINV 1
+#endif
+
 // e for pixel N of row (A, B) = R' -/+ 64 (1024 + x) through the mixed-precision FMA (exact):
 // 0xD400 = f16(-64), 0x5400 = f16(+64)
 template <bool HI, bool NEG>
@@ -1908,11 +1967,52 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_MINB_RT)
     float2 a2[8];
 #pragma unroll
     for (int n = 0; n < 8; ++n) a2[n] = f2(0.f);
+    auto err_row = [&](auto Ic, const auto& row) {
+      constexpr int I = decltype(Ic)::value;
+      using cuda::std::get;
+      const uint2 wa = lds64_reload(tile + I * TILE_W + lane * 8);
+      const uint2 wb = lds64_reload(tile + (I + 8) * TILE_W + lane * 8);
+      static_for<8>([&](auto Nc) {
+        constexpr int N = decltype(Nc)::value;
+        constexpr uint32_t sel = ((N >> 1) & 1) ? 0x4342u : 0x4140u;
+        const uint32_t ha = __byte_perm(N < 4 ? wa.x : wa.y, p.h16magic, sel);
+        const uint32_t hb = __byte_perm(N < 4 ? wb.x : wb.y, p.h16magic, sel);
+        const auto rv = get<N>(row);
+        const float2 e = err64<N, decltype(rv)::neg>(ha, hb, rv.v);  // R' - 64 (1024 + x) = R - 64 x, exact
+        a2[N] = f2fma(e, e, a2[N]);
+      });
+    };
     auto col = [&](auto Lc) {
       constexpr int L = decltype(Lc)::value;
       return inv8_sdct(FV<false>{V[0 * 8 + L]}, FV<false>{V[1 * 8 + L]}, FV<false>{V[2 * 8 + L]}, FV<false>{V[3 * 8 + L]},
                        FV<false>{V[4 * 8 + L]}, FV<false>{V[5 * 8 + L]}, FV<false>{V[6 * 8 + L]}, FV<false>{V[7 * 8 + L]});
     };
+    if constexpr (ADCT_SDCT_SINV) {
+      auto cols = [&](auto Lc, auto Bc) {
+        constexpr int L = decltype(Lc)::value, B = decltype(Bc)::value;
+        auto g = [&](int k) { return SV<false>{B ? V[k * 8 + L].y : V[k * 8 + L].x}; };
+        return inv8s_sdct(g(0), g(1), g(2), g(3), g(4), g(5), g(6), g(7), p.tab.pm1);
+      };
+      using I0 = cuda::std::integral_constant<int, 0>;
+      using I1 = cuda::std::integral_constant<int, 1>;
+      auto ua0 = cols(cuda::std::integral_constant<int, 0>{}, I0{}), ua1 = cols(cuda::std::integral_constant<int, 1>{}, I0{});
+      auto ua2 = cols(cuda::std::integral_constant<int, 2>{}, I0{}), ua3 = cols(cuda::std::integral_constant<int, 3>{}, I0{});
+      auto ua4 = cols(cuda::std::integral_constant<int, 4>{}, I0{}), ua5 = cols(cuda::std::integral_constant<int, 5>{}, I0{});
+      auto ua6 = cols(cuda::std::integral_constant<int, 6>{}, I0{}), ua7 = cols(cuda::std::integral_constant<int, 7>{}, I0{});
+      auto ub0 = cols(cuda::std::integral_constant<int, 0>{}, I1{}), ub1 = cols(cuda::std::integral_constant<int, 1>{}, I1{});
+      auto ub2 = cols(cuda::std::integral_constant<int, 2>{}, I1{}), ub3 = cols(cuda::std::integral_constant<int, 3>{}, I1{});
+      auto ub4 = cols(cuda::std::integral_constant<int, 4>{}, I1{}), ub5 = cols(cuda::std::integral_constant<int, 5>{}, I1{});
+      auto ub6 = cols(cuda::std::integral_constant<int, 6>{}, I1{}), ub7 = cols(cuda::std::integral_constant<int, 7>{}, I1{});
+      static_for<8>([&](auto Ic) {
+        constexpr int I = decltype(Ic)::value;
+        using cuda::std::get;
+        auto ra = inv8s_sdct(get<I>(ua0), get<I>(ua1), get<I>(ua2), get<I>(ua3), get<I>(ua4), get<I>(ua5), get<I>(ua6),
+                             get<I>(ua7), p.tab.pm1);
+        auto rb = inv8s_sdct(get<I>(ub0), get<I>(ub1), get<I>(ub2), get<I>(ub3), get<I>(ub4), get<I>(ub5), get<I>(ub6),
+                             get<I>(ub7), p.tab.pm1);
+        err_row(Ic, join_rows(ra, rb));
+      });
+    } else {
     auto u0 = col(cuda::std::integral_constant<int, 0>{});
     auto u1 = col(cuda::std::integral_constant<int, 1>{});
     auto u2 = col(cuda::std::integral_constant<int, 2>{});
@@ -1925,18 +2025,9 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_MINB_RT)
       constexpr int I = decltype(Ic)::value;
       using cuda::std::get;
       auto row = inv8_sdct(get<I>(u0), get<I>(u1), get<I>(u2), get<I>(u3), get<I>(u4), get<I>(u5), get<I>(u6), get<I>(u7));
-      const uint2 wa = lds64_reload(tile + I * TILE_W + lane * 8);
-      const uint2 wb = lds64_reload(tile + (I + 8) * TILE_W + lane * 8);
-      static_for<8>([&](auto Nc) {
-        constexpr int N = decltype(Nc)::value;
-        constexpr uint32_t sel = ((N >> 1) & 1) ? 0x4342u : 0x4140u;
-        const uint32_t ha = __byte_perm(N < 4 ? wa.x : wa.y, p.h16magic, sel);
-        const uint32_t hb = __byte_perm(N < 4 ? wb.x : wb.y, p.h16magic, sel);
-        const auto rv = get<N>(row);
-        const float2 e = err64<N, decltype(rv)::neg>(ha, hb, rv.v);  // R' - 64 (1024 + x) = R - 64 x, exact
-        a2[N] = f2fma(e, e, a2[N]);
-      });
+      err_row(Ic, row);
     });
+    }
     const float2 s01 = f2add(a2[0], a2[1]), s23 = f2add(a2[2], a2[3]);
     const float2 s45 = f2add(a2[4], a2[5]), s67 = f2add(a2[6], a2[7]);
     acc += fx_lane(f2add(f2add(s01, s23), f2add(s45, s67)), fxs);
