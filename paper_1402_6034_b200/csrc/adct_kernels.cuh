@@ -652,7 +652,7 @@ __device__ __forceinline__ float2 compress_quant_resid(const uint32_t (&Y)[8][8]
       else
         v[K] = f2fma(y, f2(p.tab.sq[c]), make_float2(-k.x, -k.y));
     });
-    if constexpr (SM != 0) {
+    if constexpr (SM == 1 || SM == 2) {
       float va[8], vb[8], oa[8], ob[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
