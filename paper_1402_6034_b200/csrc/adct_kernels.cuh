@@ -740,9 +740,16 @@ constexpr bool compress_grouped(int R) { return !ADCT_NOGROUP && (ADCT_GROUPED |
 #ifndef ADCT_MINB_R3
 #define ADCT_MINB_R3 3  // r = 2, 3 (3-stage ring): 4 CTAs/SM spilled (LDL/STL); 3 CTAs: r = 3 0.91 -> 0.96 of HBM (profiles/r02_variants_r3_minb.txt)
 #endif
+#ifndef ADCT_MINB_GRP
+#define ADCT_MINB_GRP 4  // grouped mid r (11 <= r < 24)
+#endif
+#ifndef ADCT_MINB_DS
+#define ADCT_MINB_DS 4  // direct scalar-butterfly form, 4 <= r <= 10
+#endif
 constexpr int compress_minb(int R) {
   // r = 64 (lossless, all 64 coefficients through the direct form): 2 CTAs/SM, no spills (4 spilled 824 B)
-  return compress_resid_r(R) ? ADCT_MINB_RESID : (R == 1 ? 6 : (R == 2 || R == 3) ? ADCT_MINB_R3 : R == 64 ? 2 : 4);
+  return compress_resid_r(R) ? ADCT_MINB_RESID
+         : (R == 1 ? 6 : (R == 2 || R == 3) ? ADCT_MINB_R3 : R == 64 ? 2 : (R >= 4 && R <= 10) ? ADCT_MINB_DS : compress_grouped(R) ? ADCT_MINB_GRP : 4);
 }
 
 #ifndef ADCT_QUANT_RING_R
