@@ -24,10 +24,10 @@ from synth import images as S  # noqa: E402
 RS = (1, 3, 6, 10, 15, 21, 28, 36)
 
 
-def load(path):
+def load(path, entry="adct_compress_psnr"):
     lib = ctypes.CDLL(path)
-    fn = lib.adct_compress_psnr
-    fn.restype, fn.argtypes = _lib.SIGNATURES["adct_compress_psnr"]
+    fn = getattr(lib, entry)
+    fn.restype, fn.argtypes = _lib.SIGNATURES[entry]
     return fn
 
 
@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--images", type=int, default=512)
     ap.add_argument("--rounds", type=int, default=7)
     ap.add_argument("--quant-frames", type=int, default=0)
+    ap.add_argument("--diag", action="store_true", help="time adct_diag_energy (Parseval sweep kernel) only")
     ap.add_argument("libs", nargs="+")
     a = ap.parse_args()
     paths = [_lib.LIB_PATH if p == "default" else p for p in a.libs]
@@ -64,6 +65,29 @@ def main():
         return [px / (statistics.median(t) * 1e-3) / 1e9 / peak for t in times]
 
     x = S.device_mixed(a.images, 4096, 4096, device="cuda")
+    if a.diag:
+        dfns = [load(p, "adct_diag_energy") for p in paths]
+        n = x.shape[0]
+        en = torch.empty((n, 16), dtype=torch.int64, device="cuda")
+        times = [[] for _ in dfns]
+        call = lambda fn: fn(x.data_ptr(), n, 4096, 4096, x.stride(1), x.stride(0), en.data_ptr(), st)
+        for fn in dfns:
+            call(fn)
+        torch.cuda.synchronize()
+        ref = en.clone()
+        for _ in range(a.rounds):
+            for i, fn in enumerate(dfns):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(3):
+                    assert call(fn) == 0
+                e1.record()
+                torch.cuda.synchronize()
+                times[i].append(e0.elapsed_time(e1) / 3)
+                assert torch.equal(en, ref), "energies differ between builds"
+        for i, p in enumerate(a.libs):
+            print(f"{os.path.basename(p):24s} diag energy HBM frac {x.numel() / (statistics.median(times[i]) * 1e-3) / 1e9 / peak:.4f}")
+        return
     fr = {r: bench(x, r, 0.0) for r in RS}
     del x
     for i, p in enumerate(a.libs):

@@ -68,6 +68,8 @@ def main():
     if hasattr(A.load(), "adct_compress_psnr_sdct"):
         add("SDCT integer fast path r=10", best_ms(lambda: A.compress_psnr_sdct(x, 10, sse=sse)), 1)
     add("dense exact DCT r=10", best_ms(lambda: A.compress_psnr_dense(x, 10, "dct", sse=sse)), 1)
+    en = torch.empty(32 * 16, dtype=torch.int64, device="cuda")
+    add("Parseval diag energy (forward + anti-diagonal energies)", best_ms(lambda: A.diag_energy(x, energy=en)), 1)
     msm = best_ms(lambda: A.compress_psnr_multi(x, (1, 3, 6, 10, 15, 21, 28, 36)))
     rows.append(("fused multi-r sweep (8 r, Gpix-passes/s)", 8 * px / (msm * 1e-3) / 1e9, px / (msm * 1e-3) / 1e9 / pk, msm))
     add("forward int16 (r=64)", best_ms(lambda: A.forward(x, out=coef)), 3)
