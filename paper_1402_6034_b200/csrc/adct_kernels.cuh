@@ -1758,8 +1758,29 @@ template <int B, int I, int L, int BLK> __device__ __forceinline__ auto band_in_
 __device__ __forceinline__ float ssub(float e, Z0) { return e; }
 __device__ __forceinline__ float ssub(float e, SV<false> r) { return e - r.v; }
 __device__ __forceinline__ float ssub(float e, SV<true> r) { return e + r.v; }
+// e - (d_n, d_{7-n}) for ONE block: the pair (e_n, e_{7-n}) minus a band's row-inverse outputs n and
+// 7 - n, which leave the same one-instruction butterfly as one register pair — one FADD2 / FFMA2 (two
+// register reads) per two pixels instead of two scalar FADDs; a sign pair from a uniform register when
+// the two outputs are stored with different signs (SV<neg>).  Exact: integers < 2^24 (R14).
+__device__ __forceinline__ float2 esub2(float2 e, Z0, Z0, float2, float2) { return e; }
+template <bool N> __device__ __forceinline__ float2 esub2(float2 e, SV<N> a, Z0, float2, float2) {
+  return make_float2(ssub(e.x, a), e.y);
+}
+template <bool N> __device__ __forceinline__ float2 esub2(float2 e, Z0, SV<N> b, float2, float2) {
+  return make_float2(e.x, ssub(e.y, b));
+}
+template <bool NA, bool NB>
+__device__ __forceinline__ float2 esub2(float2 e, SV<NA> a, SV<NB> b, float2 pm, float2 pmr) {
+  const float2 d = make_float2(a.v, b.v);
+  if constexpr (NA == NB) return NA ? f2add(e, d) : f2sub(e, d);
+  else if constexpr (NA) return __ffma2_rn(d, pm, e);  // (e.x + a, e.y - b)
+  else return __ffma2_rn(d, pmr, e);                   // (e.x - a, e.y + b)
+}
 #ifndef ADCT_SWEEP_SINV
 #define ADCT_SWEEP_SINV 1
+#endif
+#ifndef ADCT_SWEEP_PAIR
+#define ADCT_SWEEP_PAIR 1  // per-block (n, 7 - n) error pairs (esub2) in the scalar-butterfly sweep
 #endif
 
 #ifndef ADCT_INC_MINB
@@ -1812,6 +1833,41 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INC_MINB)
       constexpr int I = decltype(Ic)::value;
       const uint2 wa = lds64_reload(tile + I * TILE_W + lane * 8);
       const uint2 wb = lds64_reload(tile + (I + 8) * TILE_W + lane * 8);
+      if constexpr (ADCT_SWEEP_SINV && ADCT_SWEEP_PAIR) {
+        // eA[n] = (e_n, e_{7-n}) of block A, eB likewise (B's pixels column-mirrored under MIRB)
+        float2 eA[4], eB[4];
+        auto px576 = [&](auto Nc, bool blkb) {
+          constexpr int N = decltype(Nc)::value;
+          constexpr uint32_t sel = ((N >> 1) & 1) ? 0x4342u : 0x4140u;
+          constexpr uint32_t selb = MIRB ? (((N >> 1) & 1) ? 0x4041u : 0x4243u) : sel;
+          if (!blkb) return fhfma576<(N & 1) != 0, true>(__byte_perm(N < 4 ? wa.x : wa.y, p.h16magic, sel), -DC_BIAS16);
+          return fhfma576<(N & 1) != 0, true>(__byte_perm((N < 4) != MIRB ? wb.x : wb.y, p.h16magic, selb), -DC_BIAS16);
+        };
+        static_for<4>([&](auto Nc) {
+          constexpr int N = decltype(Nc)::value;
+          eA[N] = make_float2(px576(cuda::std::integral_constant<int, N>{}, false),
+                              px576(cuda::std::integral_constant<int, 7 - N>{}, false));
+          eB[N] = make_float2(px576(cuda::std::integral_constant<int, N>{}, true),
+                              px576(cuda::std::integral_constant<int, 7 - N>{}, true));
+        });
+        static_for<NB>([&](auto Bc) {
+          constexpr int B = decltype(Bc)::value;
+          auto ra = inv8s(band_in_s<B, I, 0, 0>(V), band_in_s<B, I, 1, 0>(V), band_in_s<B, I, 2, 0>(V),
+                          band_in_s<B, I, 3, 0>(V), band_in_s<B, I, 4, 0>(V), band_in_s<B, I, 5, 0>(V),
+                          band_in_s<B, I, 6, 0>(V), band_in_s<B, I, 7, 0>(V), p.tab.pm1);
+          auto rb = inv8s(band_in_s<B, I, 0, 1>(V), band_in_s<B, I, 1, 1>(V), band_in_s<B, I, 2, 1>(V),
+                          band_in_s<B, I, 3, 1>(V), band_in_s<B, I, 4, 1>(V), band_in_s<B, I, 5, 1>(V),
+                          band_in_s<B, I, 6, 1>(V), band_in_s<B, I, 7, 1>(V), p.tab.pm1);
+          static_for<4>([&](auto Nc) {
+            constexpr int N = decltype(Nc)::value;
+            eA[N] = esub2(eA[N], cuda::std::get<N>(ra), cuda::std::get<7 - N>(ra), p.tab.pm1, p.tab.pmr);
+            eB[N] = esub2(eB[N], cuda::std::get<N>(rb), cuda::std::get<7 - N>(rb), p.tab.pm1, p.tab.pmr);
+            acc[B] = f2fma(eA[N], eA[N], acc[B]);
+            acc[B] = f2fma(eB[N], eB[N], acc[B]);
+          });
+        });
+        return;
+      }
       float2 e[8];  // 576 x - R of this output row, R over the bands added so far (none yet)
       static_for<8>([&](auto Nc) {
         constexpr int N = decltype(Nc)::value;
