@@ -1,0 +1,4 @@
+python -m pytest tests -q -m gpu 2>&1 | tail -3 > gpurun_out/r02_gputests15.txt
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02_smoke.txt 2>&1
+python bench.py --steps 10 --warmup 3 > gpurun_out/r02_bench6.jsonl 2> gpurun_out/r02_bench6.err
+python bench.py > gpurun_out/r02_bench6_default.jsonl 2> gpurun_out/r02_bench6_default.err
