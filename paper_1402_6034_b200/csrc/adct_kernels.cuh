@@ -1866,42 +1866,42 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INC_MINB)
             acc[B] = f2fma(eB[N], eB[N], acc[B]);
           });
         });
-        return;
+      } else {  // (block A, block B) pairs: two scalar FADDs per pixel pair and band
+        float2 e[8];  // 576 x - R of this output row, R over the bands added so far (none yet)
+        static_for<8>([&](auto Nc) {
+          constexpr int N = decltype(Nc)::value;
+          // 576 (1024 + x) - 589824 = 576 x through the mixed-precision FMA (exact)
+          constexpr uint32_t sel = ((N >> 1) & 1) ? 0x4342u : 0x4140u;
+          constexpr uint32_t selb = MIRB ? (((N >> 1) & 1) ? 0x4041u : 0x4243u) : sel;
+          const uint32_t ha = __byte_perm(N < 4 ? wa.x : wa.y, p.h16magic, sel);
+          const uint32_t hb = __byte_perm((N < 4) != MIRB ? wb.x : wb.y, p.h16magic, selb);
+          e[N] = make_float2(fhfma576<(N & 1) != 0, true>(ha, -DC_BIAS16), fhfma576<(N & 1) != 0, true>(hb, -DC_BIAS16));
+        });
+        static_for<NB>([&](auto Bc) {
+          constexpr int B = decltype(Bc)::value;
+          if constexpr (ADCT_SWEEP_SINV) {  // per block, one-instruction butterflies (inv8s)
+            auto ra = inv8s(band_in_s<B, I, 0, 0>(V), band_in_s<B, I, 1, 0>(V), band_in_s<B, I, 2, 0>(V),
+                            band_in_s<B, I, 3, 0>(V), band_in_s<B, I, 4, 0>(V), band_in_s<B, I, 5, 0>(V),
+                            band_in_s<B, I, 6, 0>(V), band_in_s<B, I, 7, 0>(V), p.tab.pm1);
+            auto rb = inv8s(band_in_s<B, I, 0, 1>(V), band_in_s<B, I, 1, 1>(V), band_in_s<B, I, 2, 1>(V),
+                            band_in_s<B, I, 3, 1>(V), band_in_s<B, I, 4, 1>(V), band_in_s<B, I, 5, 1>(V),
+                            band_in_s<B, I, 6, 1>(V), band_in_s<B, I, 7, 1>(V), p.tab.pm1);
+            static_for<8>([&](auto Nc) {
+              constexpr int N = decltype(Nc)::value;
+              e[N] = make_float2(ssub(e[N].x, cuda::std::get<N>(ra)), ssub(e[N].y, cuda::std::get<N>(rb)));
+              acc[B] = f2fma(e[N], e[N], acc[B]);
+            });
+          } else {
+            auto row = inv8(band_in<B, I, 0>(V), band_in<B, I, 1>(V), band_in<B, I, 2>(V), band_in<B, I, 3>(V),
+                            band_in<B, I, 4>(V), band_in<B, I, 5>(V), band_in<B, I, 6>(V), band_in<B, I, 7>(V));
+            static_for<8>([&](auto Nc) {
+              constexpr int N = decltype(Nc)::value;
+              e[N] = rsub(e[N], cuda::std::get<N>(row));  // e_{r_B} = e_{r_{B-1}} - dR_B, exact
+              acc[B] = f2fma(e[N], e[N], acc[B]);
+            });
+          }
+        });
       }
-      float2 e[8];  // 576 x - R of this output row, R over the bands added so far (none yet)
-      static_for<8>([&](auto Nc) {
-        constexpr int N = decltype(Nc)::value;
-        // 576 (1024 + x) - 589824 = 576 x through the mixed-precision FMA (exact)
-        constexpr uint32_t sel = ((N >> 1) & 1) ? 0x4342u : 0x4140u;
-        constexpr uint32_t selb = MIRB ? (((N >> 1) & 1) ? 0x4041u : 0x4243u) : sel;
-        const uint32_t ha = __byte_perm(N < 4 ? wa.x : wa.y, p.h16magic, sel);
-        const uint32_t hb = __byte_perm((N < 4) != MIRB ? wb.x : wb.y, p.h16magic, selb);
-        e[N] = make_float2(fhfma576<(N & 1) != 0, true>(ha, -DC_BIAS16), fhfma576<(N & 1) != 0, true>(hb, -DC_BIAS16));
-      });
-      static_for<NB>([&](auto Bc) {
-        constexpr int B = decltype(Bc)::value;
-        if constexpr (ADCT_SWEEP_SINV) {  // per block, one-instruction butterflies (inv8s)
-          auto ra = inv8s(band_in_s<B, I, 0, 0>(V), band_in_s<B, I, 1, 0>(V), band_in_s<B, I, 2, 0>(V),
-                          band_in_s<B, I, 3, 0>(V), band_in_s<B, I, 4, 0>(V), band_in_s<B, I, 5, 0>(V),
-                          band_in_s<B, I, 6, 0>(V), band_in_s<B, I, 7, 0>(V), p.tab.pm1);
-          auto rb = inv8s(band_in_s<B, I, 0, 1>(V), band_in_s<B, I, 1, 1>(V), band_in_s<B, I, 2, 1>(V),
-                          band_in_s<B, I, 3, 1>(V), band_in_s<B, I, 4, 1>(V), band_in_s<B, I, 5, 1>(V),
-                          band_in_s<B, I, 6, 1>(V), band_in_s<B, I, 7, 1>(V), p.tab.pm1);
-          static_for<8>([&](auto Nc) {
-            constexpr int N = decltype(Nc)::value;
-            e[N] = make_float2(ssub(e[N].x, cuda::std::get<N>(ra)), ssub(e[N].y, cuda::std::get<N>(rb)));
-            acc[B] = f2fma(e[N], e[N], acc[B]);
-          });
-        } else {
-          auto row = inv8(band_in<B, I, 0>(V), band_in<B, I, 1>(V), band_in<B, I, 2>(V), band_in<B, I, 3>(V),
-                          band_in<B, I, 4>(V), band_in<B, I, 5>(V), band_in<B, I, 6>(V), band_in<B, I, 7>(V));
-          static_for<8>([&](auto Nc) {
-            constexpr int N = decltype(Nc)::value;
-            e[N] = rsub(e[N], cuda::std::get<N>(row));  // e_{r_B} = e_{r_{B-1}} - dR_B, exact
-            acc[B] = f2fma(e[N], e[N], acc[B]);
-          });
-        }
-      });
     });
 #pragma unroll
     for (int b = 0; b < NB; ++b) dacc[b] += fx_lane(acc[b], fxs);
