@@ -92,6 +92,20 @@ def test_forward_c1_and_c3_subset_bit_exact():
     assert np.array_equal(Y, O.forward_int(host(x)))
 
 
+def test_forward_c3_full_size_bench_launch_sampled():
+    """C3 in the launch configuration bench.py times: 8192 x 512^2 uniform images (2 GiB) -> int16
+    (4 GiB) in ONE call; sampled images across the batch bit-exact against the oracle."""
+    x = S.device_uniform(8192, 512, 512, seed=0)
+    out = torch.empty((8192, 512, 512), dtype=torch.int16, device="cuda")
+    A.forward(x, out=out)
+    sample = [0, 1, 4095, 4096, 8190, 8191]
+    Y = host(out[sample]).astype(np.int64)
+    imgs = host(x[sample])
+    del x, out
+    torch.cuda.empty_cache()
+    assert np.array_equal(Y, O.forward_int(imgs))
+
+
 def test_forward_pitch_and_image_stride():
     base = torch.zeros((3, 40, 96), dtype=torch.uint8, device="cuda")
     imgs = rng.integers(0, 256, (3, 32, 64), dtype=np.uint8)
@@ -247,20 +261,30 @@ def test_compress_c5_pattern_blocks_closed_form():
 
 def test_compress_c5_full_size_bench_launch_sampled():
     """C5 at full size (4096 x 4096^2 = 64 GiB, the launch configuration bench.py times):
-    sampled images across the corpus (all three kinds, first / middle / last chunks) vs the oracle,
-    and every image's SSE non-increasing in r."""
+    sampled images across the corpus (all three kinds, first / middle / last chunks) vs the oracle
+    at r = 1, 10, 36, the first and last image at the other five C5 r, every image's SSE
+    non-increasing in r, and the fused multi-r kernel on the same corpus equal to the passes."""
     n = 4096
     x = S.device_mixed(n, 4096, 4096, seed=0)
     sample = [0, 1, 2, 2047, 2048, 4093, 4094, 4095]
+    rs = (1, 3, 6, 10, 15, 21, 28, 36)
+    per_r = {}
     prev = None
-    for r in (1, 10, 36):
+    for r in rs:
         sse = host(A.compress_psnr(x, r))
         assert np.all(np.isfinite(sse)) and np.all(sse > 0)
-        imgs = host(x[sample])
-        check_sse(sse[sample], O.compress_zonal_sse(imgs, r), 4096 * 4096)
+        if r in (1, 10, 36):
+            check_sse(sse[sample], O.compress_zonal_sse(host(x[sample]), r), 4096 * 4096)
+        else:  # the other C5 r: the first and the last image of the corpus
+            check_sse(sse[[0, 4095]], O.compress_zonal_sse(host(x[[0, 4095]]), r), 4096 * 4096)
         if prev is not None:
             assert np.all(sse <= prev * (1 + 1e-6))
-        prev = sse
+        prev = per_r[r] = sse
+    # the fused multi-r line (bench's fused_multi_r_c5) in its launch configuration: every image,
+    # every r, against the independent passes
+    got = host(A.compress_psnr_multi(x, rs))
+    for k, r in enumerate(rs):
+        assert np.allclose(got[k], per_r[r], rtol=SSE_RTOL, atol=0), r
     del x
     torch.cuda.empty_cache()
 
@@ -364,12 +388,17 @@ def test_compress_quant_c4_constant_frames_closed_form():
 
 
 def test_compress_quant_c4_frames_vs_oracle():
-    """C4: frames 0, 60, 120, 180 of the video recipe at full 4320 x 7680 size, q = 16."""
-    for t in (0, 60, 120, 180):
-        x = S.device_video(1, 4320, 7680, seed=0, first_frame=t)
-        imgs = host(x)
-        sse = host(A.compress_psnr(x, 64, q=16.0))
-        check_sse(sse, O.compress_quant_sse(imgs, 16.0), 4320 * 7680)
+    """C4 in the launch configuration bench.py times: all 240 frames of the video recipe
+    (4320 x 7680, 7.96 GB) in ONE q = 16 call; frames 0, 120 and 239 against the oracle, every
+    frame's SSE finite and positive."""
+    x = S.device_video(240, 4320, 7680, seed=0)
+    sse = host(A.compress_psnr(x, 64, q=16.0))
+    assert np.all(np.isfinite(sse)) and np.all(sse > 0)
+    sample = [0, 120, 239]
+    imgs = host(x[sample])
+    del x
+    torch.cuda.empty_cache()
+    check_sse(sse[sample], O.compress_quant_sse(imgs, 16.0), 4320 * 7680)
 
 
 # ------------------------------------------------------------------ ABI behaviour on the device
