@@ -567,6 +567,7 @@ adct_status adct_compress_sse576(const uint8_t* src, int64_t n, int64_t h, int64
   p.h = (int)h;
   p.w = (int)w;
   p.sse576 = reinterpret_cast<unsigned long long*>(sse576);
+  p.h16magic = 0x64646464u;  // f16 pixel pairs of the error route (k_compress_exact)
   fill_zonal_tables(p.tab, r);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(sse576, 0, sizeof(uint64_t) * (size_t)n, s);
