@@ -147,6 +147,7 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.samples, self.reasons, self.stop_ev = [], set(), threading.Event()
+        self.power = []
         self.max_mhz = None
         try:
             import pynvml
@@ -162,6 +163,7 @@ class ClockSampler:
         while not self.stop_ev.is_set():
             try:
                 self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.power.append(self.nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
                 mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
                 for name, bit in self.REASONS.items():
                     if mask & bit:
@@ -182,8 +184,11 @@ class ClockSampler:
 
     def summary(self):
         med = statistics.median(self.samples) if self.samples else None
-        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.samples)}
+        out = {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+               "samples": len(self.samples)}
+        if self.power:  # board power (W): the compute-bound passes run at the power-capped clock
+            out["power_w_median"] = statistics.median(self.power)
+        return out
 
 
 def _oracle_image_task(args):
