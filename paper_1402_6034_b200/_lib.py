@@ -36,6 +36,7 @@ SIGNATURES = {
     "adct_uqi": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _vp, _vp]),
     "adct_transform_matrix": (_i32, [_i32, _vp]),
     "adct_diag_energy": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp]),
+    "adct_diag_energy_prefix": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _vp]),
     "adct_compress_psnr_sdct": (_i32, [_vp, _i64, _i64, _i64, _i64, _i64, _i32, _vp, _vp]),
     "adct_sweep_psnr": (_i32, [_vp, _i64, _i64, _vp, _i32, _vp, _vp, _vp]),
     "adct_status_string": (ctypes.c_char_p, [_i32]),
@@ -182,14 +183,20 @@ def uqi(x, y, out=None, stream=None):
     return out
 
 
-def diag_energy(x, energy=None, stream=None):
-    """adct_diag_energy: exact per-image anti-diagonal energies sum W Y^2 (uint64 [n, 16], device)."""
+def diag_energy(x, energy=None, stream=None, r_max: int = 64):
+    """adct_diag_energy (r_max = 64) / adct_diag_energy_prefix: exact per-image anti-diagonal
+    energies sum W Y^2 in entries 0..14 and the block energy 576 sum x^2 in entry 15 (uint64 [n, 16],
+    device); with r_max <= 36 only anti-diagonals 0..7 are computed (the others hold UINT64_MAX)."""
     torch = _torch()
     p, n, h, w, pitch, istr = _plane(x, 1)
     if energy is None:
         energy = torch.empty((n, 16), dtype=torch.int64, device=x.device)
-    _check(load().adct_diag_energy(p, n, h, w, pitch, istr, energy.data_ptr(), _stream(stream)),
-           "adct_diag_energy")
+    if r_max == 64:
+        _check(load().adct_diag_energy(p, n, h, w, pitch, istr, energy.data_ptr(), _stream(stream)),
+               "adct_diag_energy")
+    else:
+        _check(load().adct_diag_energy_prefix(p, n, h, w, pitch, istr, int(r_max), energy.data_ptr(),
+                                              _stream(stream)), "adct_diag_energy_prefix")
     return energy
 
 

@@ -785,8 +785,11 @@ adct_status adct_compress_psnr_sdct(const uint8_t* src, int64_t n, int64_t h, in
   return fx_finish(sse, n, fxk, s);
 }
 
-adct_status adct_diag_energy(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch, int64_t img_stride,
-                             uint64_t* energy, adct_stream_t stream) {
+}  // extern "C"
+namespace {
+// anti-diagonal energies of every image; SMAX = 14 (all) or 7 (r <= 36: slots 8..14 = UINT64_MAX)
+adct_status diag_energy_impl(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch, int64_t img_stride,
+                             int smax, uint64_t* energy, cudaStream_t s) {
   adct_status st = check_geom(n, h, w);
   if (st) return st;
   if (!energy) return ADCT_EINVAL;
@@ -801,10 +804,26 @@ adct_status adct_diag_energy(const uint8_t* src, int64_t n, int64_t h, int64_t w
   p.h = (int)h;
   p.w = (int)w;
   p.energy = reinterpret_cast<unsigned long long*>(energy);
-  cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(energy, 0, sizeof(uint64_t) * 16 * (size_t)n, s);
+  if (e == cudaSuccess && smax < 14)  // not computed: UINT64_MAX (adct_sweep_psnr answers NaN)
+    e = cudaMemset2DAsync(energy + smax + 1, 16 * sizeof(uint64_t), 0xFF, (14 - smax) * sizeof(uint64_t),
+                          (size_t)n, s);
   if (e != cudaSuccess) return cuda_fail(e);
-  return launch_tma_kernel(k_diag_energy<0>, map, p, p.tiles, s, DIAG_ST);
+  return smax == 14 ? launch_tma_kernel(k_diag_energy<14>, map, p, p.tiles, s, DIAG_ST)
+                    : launch_tma_kernel(k_diag_energy<7>, map, p, p.tiles, s, DIAG_ST);
+}
+}  // namespace
+extern "C" {
+
+adct_status adct_diag_energy(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch, int64_t img_stride,
+                             uint64_t* energy, adct_stream_t stream) {
+  return diag_energy_impl(src, n, h, w, pitch, img_stride, 14, energy, (cudaStream_t)stream);
+}
+
+adct_status adct_diag_energy_prefix(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
+                                    int64_t img_stride, int r_max, uint64_t* energy, adct_stream_t stream) {
+  if (r_max < 1 || r_max > 64) return ADCT_EINVAL;
+  return diag_energy_impl(src, n, h, w, pitch, img_stride, r_max <= 36 ? 7 : 14, energy, (cudaStream_t)stream);
 }
 
 adct_status adct_sweep_psnr(const uint64_t* energy, int64_t n, int64_t pixels, const int* r_list, int n_r, double* sse,

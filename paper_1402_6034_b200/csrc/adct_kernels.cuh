@@ -1505,7 +1505,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3)
 // of its discarded orthonormal coefficients: 576^2 SSE = 576 * sum_{zz >= r} W Y^2 with
 // W = 576 / (d_i d_j).  The kernel accumulates, per image, the exact integer energy
 // E_s = sum_blocks sum_{k+l=s} W_kl Y_kl^2 of each anti-diagonal s = 0..14 (u64); for a
-// triangular r = (s+1)(s+2)/2 the SSE is sum_{s' > s} E_s' / 576.  No inverse is computed, so this
+// triangular r = (s+1)(s+2)/2 the SSE is sum_{s' > s} E_s' / 576 = (E_total - sum_{s' <= s} E_s') / 576.  No inverse is computed, so this
 // is NOT the fwd+zonal+inv path of the headline metric and is reported separately.
 // ------------------------------------------------------------------------------------------
 struct DiagParams {
@@ -1543,25 +1543,32 @@ constexpr int diag_group(int k, int l) {
 #define ADCT_DIAG_MINB 3
 #endif
 constexpr int DIAG_ST = ADCT_DIAG_ST, DIAG_MINB = ADCT_DIAG_MINB;  // ring depth, CTAs per SM (measured: 2/3 best, 0.53 vs 0.46 of HBM for 3/4)
-template <int UNUSED = 0>
+// SMAX: the last anti-diagonal computed (14 = all; 7 = the triangular r <= 36 of C5, whose forward
+// prunes the 28 coefficients of anti-diagonals 8..14).  Slot 15 of every image receives the block
+// energy sum_all W Y^2 = 576 sum x^2 (P9 at r = 64: R = 576 x), from the pixels with one IDP4A per
+// four (exact u32 per tile: 128 x 255^2 < 2^24), so SSE(r_s) = (E_15 - sum_{s' <= s} E_s') / 576
+// needs only the anti-diagonals up to s.
+template <int SMAX = 14>
 __global__ void __launch_bounds__(WARPS * 32, DIAG_MINB)
     k_diag_energy(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ DiagParams p) {
+  static_assert(SMAX >= 0 && SMAX <= 14, "anti-diagonals 0..14");
+  constexpr int NS = SMAX + 1, RC = SMAX <= 7 ? (SMAX + 1) * (SMAX + 2) / 2 : 64;  // RC: zig-zag prefix
   extern __shared__ __align__(128) uint8_t smem[];
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   uint8_t* ring = smem + warp * (DIAG_ST * TILE_BYTES);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + WARPS * DIAG_ST * TILE_BYTES) + warp * DIAG_ST;
   const StepPlan plan = make_step_plan(p.geo, p.tiles, p.cshift, (int)gridDim.x * WARPS);
   int cur = -1;
-  long long E[15];
+  long long E[NS + 1];  // E[NS]: 576 sum x^2 (slot 15)
 #pragma unroll
-  for (int s = 0; s < 15; ++s) E[s] = 0;
+  for (int s = 0; s <= NS; ++s) E[s] = 0;
   auto flush = [&](int img) {
 #pragma unroll
-    for (int s = 0; s < 15; ++s) {
+    for (int s = 0; s <= NS; ++s) {
       long long v = E[s];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      if (lane == 0 && img >= 0) atomicAdd(p.energy + (int64_t)img * 16 + s, (unsigned long long)v);
+      if (lane == 0 && img >= 0) atomicAdd(p.energy + (int64_t)img * 16 + (s == NS ? 15 : s), (unsigned long long)v);
       E[s] = 0;
     }
   };
@@ -1571,28 +1578,38 @@ __global__ void __launch_bounds__(WARPS * 32, DIAG_MINB)
       cur = img;
     }
     uint32_t P[8][8];
+    uint32_t x2 = 0u;  // sum of the 128 squared pixels of this lane's block pair (IDP4A)
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
-      pack_rows(lds64(tile + i * TILE_W + lane * 8), lds64(tile + (i + 8) * TILE_W + lane * 8), P[i]);
+    for (int i = 0; i < 8; ++i) {
+      const uint2 wa = lds64(tile + i * TILE_W + lane * 8), wb = lds64(tile + (i + 8) * TILE_W + lane * 8);
+      x2 = __dp4a(wa.x, wa.x, x2);
+      x2 = __dp4a(wa.y, wa.y, x2);
+      x2 = __dp4a(wb.x, wb.x, x2);
+      x2 = __dp4a(wb.y, wb.y, x2);
+      pack_rows(wa, wb, P[i]);
+    }
+    E[NS] += 576ll * (long long)x2;
     uint32_t Y[8][8];
-    fwd2d<0u, 64>(P, Y);  // unbiased: lo lane = Y_A (two's complement), P - Y_A = Y_B * 2^16 exactly
+    fwd2d<0u, RC>(P, Y);  // unbiased: lo lane = Y_A (two's complement), P - Y_A = Y_B * 2^16 exactly
     // Per tile, exact u32 sums of Y^2 per (anti-diagonal s, weight W) group — 28 groups, at most 4
     // positions x 2 blocks each, so a sum stays below 8 * 16320^2 < 2^32 — then one 64-bit
     // multiply-add E_s += W * S per group.  Per coefficient pair: Y_A = sext16 (PRMT), Y_A^2 (IMAD),
     // d = P - Y_A = Y_B 2^16 (IADD), Y_B^2 = hi(d * d) (IMAD.HI): 2 ALU + 2 FMA-pipe instructions.
-    uint32_t S[15][4];
-    static_for<15>([&](auto Sc) {
+    uint32_t S[NS][4];
+    static_for<NS>([&](auto Sc) {
       static_for<4>([&](auto Gc) { S[decltype(Sc)::value][decltype(Gc)::value] = 0u; });
     });
     static_for<64>([&](auto KLc) {
       constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
-      constexpr int g = diag_group(k, l);
-      const uint32_t w = Y[k][l];
-      const int a = (int)(int16_t)(w & 0xFFFFu);      // sign-extended low lane: Y of block A
-      const int d = (int)(w - (uint32_t)a);           // Y of block B times 2^16
-      S[k + l][g] += (uint32_t)(a * a) + (uint32_t)__mulhi(d, d);
+      if constexpr (k + l <= SMAX) {
+        constexpr int g = diag_group(k, l);
+        const uint32_t w = Y[k][l];
+        const int a = (int)(int16_t)(w & 0xFFFFu);      // sign-extended low lane: Y of block A
+        const int d = (int)(w - (uint32_t)a);           // Y of block B times 2^16
+        S[k + l][g] += (uint32_t)(a * a) + (uint32_t)__mulhi(d, d);
+      }
     });
-    static_for<15>([&](auto Sc) {
+    static_for<NS>([&](auto Sc) {
       constexpr int sd = decltype(Sc)::value;
       static_for<4>([&](auto Gc) {
         constexpr int g = decltype(Gc)::value;
@@ -1616,11 +1633,19 @@ __global__ void k_sweep_psnr(const unsigned long long* __restrict__ energy, int6
   if (i >= n * L.n_r) return;
   const int64_t img = i % n;
   const int k = (int)(i / n);
-  unsigned long long acc = 0;
-  for (int s = L.diag[k] + 1; s < 15; ++s) acc += energy[img * 16 + s];
+  // SSE(r_s) = (E_15 - sum_{s' <= s} E_s') / 576 with E_15 = sum_all W Y^2 = 576 sum x^2 (exact in
+  // u64); an anti-diagonal the energy kernel did not compute (UINT64_MAX) makes the result NaN
+  unsigned long long acc = energy[img * 16 + 15];
+  bool missing = false;
+  for (int s = 0; s <= L.diag[k]; ++s) {
+    const unsigned long long v = energy[img * 16 + s];
+    missing = missing || v == ~0ull;
+    acc -= v;
+  }
   const double e = (double)acc / 576.0;
-  sse[i] = e;
-  psnr[i] = (acc == 0) ? __longlong_as_double(0x7ff0000000000000ll) : 10.0 * log10(65025.0 * pixels / e);
+  const double nan = __longlong_as_double(0x7ff8000000000000ll);
+  sse[i] = missing ? nan : e;
+  psnr[i] = missing ? nan : (acc == 0) ? __longlong_as_double(0x7ff0000000000000ll) : 10.0 * log10(65025.0 * pixels / e);
 }
 
 // ------------------------------------------------------------------------------------------

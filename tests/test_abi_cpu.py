@@ -21,7 +21,7 @@ def header_functions():
 def test_library_exports_every_declared_symbol():
     lib = A.load()
     names = header_functions()
-    assert len(names) == 18
+    assert len(names) == 19
     for name in names:
         assert hasattr(lib, name), name
         assert name in _lib.SIGNATURES, name
@@ -154,6 +154,8 @@ def test_sweep_validation():
     rl = (ctypes.c_int * 1)(10)
     assert lib.adct_sweep_psnr(16, 0, 64, rl, 1, 32, 48, None) == E
     assert lib.adct_diag_energy(16, 1, 8, 16, 16, 128, 0, None) == E
+    for r_max in (0, 65):  # the prefix entry validates r_max before anything else
+        assert lib.adct_diag_energy_prefix(16, 1, 8, 16, 16, 128, r_max, 32, None) == E
 
 
 def test_multi_and_geometry_limits_validation():

@@ -556,6 +556,9 @@ def test_diag_energy_bit_exact_and_sweep_sse():
     E = host(A.diag_energy(x))
     want = oracle_diag_energy(imgs)
     assert np.array_equal(E[:, :15].astype(np.int64), want)
+    # entry 15: the block energy 576 sum x^2, equal to the oracle's 15 energies summed (Parseval, P9)
+    assert np.array_equal(E[:, 15].astype(np.int64), want.sum(axis=1))
+    assert np.array_equal(E[:, 15].astype(np.int64), 576 * (imgs.astype(np.int64) ** 2).sum(axis=(1, 2)))
     rs = [1, 3, 6, 10, 15, 21, 28, 36, 43, 49, 54, 58, 61, 63, 64]
     sse, ps = A.sweep_psnr(A.diag_energy(x), 64 * 96, rs)
     sse = host(sse)
@@ -590,11 +593,39 @@ def test_extreme_aspect_ratios_every_entry(h, w):
         check_sse(multi[k], exact / 576.0 ** 2, h * w)
 
 
+def test_diag_energy_prefix_and_sweep():
+    """adct_diag_energy_prefix (r_max <= 36): anti-diagonals 0..7 and the block energy bit-exact
+    against the oracle, 8..14 marked UINT64_MAX; the sweep from it equals the full one for every
+    r <= 36 and is NaN beyond; r_max > 36 falls back to every anti-diagonal."""
+    imgs = np.concatenate([S.corpus_c2(3, 64, 96), rng.integers(0, 256, (1, 64, 96), dtype=np.uint8),
+                           np.full((1, 64, 96), 255, dtype=np.uint8)])
+    x = dev(imgs)
+    want = oracle_diag_energy(imgs)
+    full = A.diag_energy(x)
+    for r_max in (1, 10, 36):
+        E = A.diag_energy(x, r_max=r_max)
+        Eh = host(E)
+        assert np.array_equal(Eh[:, :8].astype(np.int64), want[:, :8]), r_max
+        assert np.all(Eh[:, 8:15] == -1), r_max                      # UINT64_MAX as int64
+        assert np.array_equal(Eh[:, 15].astype(np.int64), want.sum(axis=1)), r_max
+        rs = [1, 3, 6, 10, 15, 21, 28, 36]
+        a, pa = A.sweep_psnr(E, 64 * 96, rs)
+        b, pb = A.sweep_psnr(full, 64 * 96, rs)
+        assert torch.equal(a, b) and torch.equal(pa, pb), r_max
+        nan_sse, nan_ps = A.sweep_psnr(E, 64 * 96, [43, 64])
+        assert torch.isnan(nan_sse).all() and torch.isnan(nan_ps).all()
+    assert np.array_equal(host(A.diag_energy(x, r_max=43)), host(full))
+
+
 def test_diag_energy_c5_full_size_sampled():
     x = S.device_mixed(64, 4096, 4096, seed=1)
     E = host(A.diag_energy(x))
     sample = [0, 1, 2, 63]
-    assert np.array_equal(E[sample, :15].astype(np.int64), oracle_diag_energy(host(x[sample])))
+    want = oracle_diag_energy(host(x[sample]))
+    assert np.array_equal(E[sample, :15].astype(np.int64), want)
+    assert np.array_equal(E[sample, 15].astype(np.int64), want.sum(axis=1))
+    Ep = host(A.diag_energy(x, r_max=36))  # the bench's Parseval-sweep call
+    assert np.array_equal(Ep[:, :8], E[:, :8]) and np.array_equal(Ep[:, 15], E[:, 15])
 
 
 # ------------------------------------------------------------------ UQI / APE (F2)
