@@ -355,7 +355,7 @@ const char* adct_status_string(adct_status s) {
 }
 
 int adct_last_cuda_error(void) { return g_last_cuda; }
-int adct_version(void) { return 10100; }
+int adct_version(void) { return 10200; }
 int64_t adct_launch_count(void) { return g_launches; }
 
 adct_status adct_forward(const uint8_t* src, int64_t n, int64_t h, int64_t w, int64_t pitch,
