@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--rounds", type=int, default=7)
     ap.add_argument("--quant-frames", type=int, default=0)
     ap.add_argument("--diag", action="store_true", help="time adct_diag_energy (Parseval sweep kernel) only")
+    ap.add_argument("--rs", default=None, help="comma-separated r values instead of C5's eight")
     ap.add_argument("libs", nargs="+")
     a = ap.parse_args()
     paths = [_lib.LIB_PATH if p == "default" else p for p in a.libs]
@@ -88,11 +89,12 @@ def main():
         for i, p in enumerate(a.libs):
             print(f"{os.path.basename(p):24s} diag energy HBM frac {x.numel() / (statistics.median(times[i]) * 1e-3) / 1e9 / peak:.4f}")
         return
-    fr = {r: bench(x, r, 0.0) for r in RS}
+    rs = tuple(int(v) for v in a.rs.split(",")) if a.rs else RS
+    fr = {r: bench(x, r, 0.0) for r in rs}
     del x
     for i, p in enumerate(a.libs):
-        tot = len(RS) / sum(1 / fr[r][i] for r in RS)
-        print(f"{os.path.basename(p):24s} step-equivalent {tot:.4f} | " + " ".join(f"r{r}:{fr[r][i]:.3f}" for r in RS))
+        tot = len(rs) / sum(1 / fr[r][i] for r in rs)
+        print(f"{os.path.basename(p):24s} step-equivalent {tot:.4f} | " + " ".join(f"r{r}:{fr[r][i]:.3f}" for r in rs))
     if a.quant_frames:
         v = S.device_video(a.quant_frames, 4320, 7680, seed=0, device="cuda")
         fq = bench(v, 64, 16.0)
