@@ -709,9 +709,11 @@ __device__ __forceinline__ float2 compress_quant_resid(const uint32_t (&Y)[8][8]
 // ------------------------------------------------------------------------------------------
 // measured on B200 (profiles/r01_tune_compress.txt): small r wants occupancy, large r registers
 constexpr int compress_stages(int R) { return (R == 2 || R == 3) ? 3 : 2; }  // r = 2, 3: HBM-side bound
-// residual form from this r on: cheaper once the discarded set is the smaller one
+// residual form from this r on: cheaper once the discarded set is the smaller one;
+// measured with the scalar-butterfly residual (profiles/r02_variants_resid_from.txt): r = 23 residual
+// 0.615 vs direct 0.546 of HBM, r = 22 equal, r <= 21 direct
 #ifndef ADCT_RESID_FROM
-#define ADCT_RESID_FROM 24
+#define ADCT_RESID_FROM 23
 #endif
 constexpr int compress_resid_r(int R) { return R >= ADCT_RESID_FROM && R < 64; }
 // output rows per tile that take the f16 error route (ALU -> FMA pipe rebalancing, compress_inv)
@@ -741,7 +743,7 @@ constexpr bool compress_grouped(int R) { return !ADCT_NOGROUP && (ADCT_GROUPED |
 #define ADCT_MINB_R3 3  // r = 2, 3 (3-stage ring): 4 CTAs/SM spilled (LDL/STL); 3 CTAs: r = 3 0.91 -> 0.96 of HBM (profiles/r02_variants_r3_minb.txt)
 #endif
 #ifndef ADCT_MINB_GRP
-#define ADCT_MINB_GRP 4  // grouped mid r (11 <= r < 24)
+#define ADCT_MINB_GRP 4  // grouped mid r (11 <= r < ADCT_RESID_FROM)
 #endif
 #ifndef ADCT_MINB_DS
 #define ADCT_MINB_DS 4  // direct scalar-butterfly form, 4 <= r <= 10
@@ -769,7 +771,7 @@ constexpr int compress_minb(int R) {
 #define ADCT_HYB_HI 18
 #endif
 // measured per r (profiles/r02_variants_inverse_flavour*.txt, r02_variants_hybrid_mid_r.txt): scalar
-// butterflies for the ungrouped direct form (r <= 10) and the residual form (r >= 24), the hybrid
+// butterflies for the ungrouped direct form (r <= 10) and the residual form (r >= 23), the hybrid
 // (f32x2 columns, scalar rows) for the grouped r = 12..18 (+2-5 %), f32x2 for the other grouped r
 // (r = 20, 21: the hybrid loses 2-4 %) and the quantiser
 constexpr int sinv_mode(int R, int MODE, int RECON) {
