@@ -770,13 +770,15 @@ constexpr int compress_minb(int R) {
 #ifndef ADCT_HYB_HI
 #define ADCT_HYB_HI 18
 #endif
-// measured per r (profiles/r02_variants_inverse_flavour*.txt, r02_variants_hybrid_mid_r.txt): scalar
-// butterflies for the ungrouped direct form (r <= 10) and the residual form (r >= 23), the hybrid
+// measured per r (profiles/r02_variants_inverse_flavour*.txt, r02_variants_hybrid_mid_r.txt,
+// r02_variants_low_high_r.txt): scalar butterflies for the ungrouped direct form (r <= 10, except
+// r = 2-4, 7, 8 where f32x2 is 1-4 % faster) and the residual form (r >= 23: +6-9 %), the hybrid
 // (f32x2 columns, scalar rows) for the grouped r = 12..18 (+2-5 %), f32x2 for the other grouped r
 // (r = 20, 21: the hybrid loses 2-4 %) and the quantiser
 constexpr int sinv_mode(int R, int MODE, int RECON) {
   return ADCT_SINV >= 0 ? ADCT_SINV
-         : (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT && !compress_grouped(R))                ? 1
+         : (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT && !compress_grouped(R) &&
+            !(R >= 2 && R <= 4) && R != 7 && R != 8)                                               ? 1
          : (MODE == MODE_ZONAL && RECON == REC_NONE && compress_grouped(R) && R >= ADCT_HYB_LO && R <= ADCT_HYB_HI)
              ? 3
              : 0;
