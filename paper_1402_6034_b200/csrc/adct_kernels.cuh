@@ -1856,6 +1856,14 @@ template <int B, int I, int L, int BLK> __device__ __forceinline__ auto band_in_
   else if constexpr (c0_entry(k, I) > 0) return SV<false>{BLK ? V[k * 8 + L].y : V[k * 8 + L].x};
   else return SV<true>{BLK ? V[k * 8 + L].y : V[k * 8 + L].x};
 }
+// the same from a per-block scalar plane (the split sweep)
+template <int B, int I, int L> __device__ __forceinline__ auto band_in_v(const float (&VS)[64]) {
+  constexpr int k = B - L;
+  if constexpr (k < 0 || k > 7) return Z0{};
+  else if constexpr (c0_entry(k, I) == 0) return Z0{};
+  else if constexpr (c0_entry(k, I) > 0) return SV<false>{VS[k * 8 + L]};
+  else return SV<true>{VS[k * 8 + L]};
+}
 __device__ __forceinline__ float ssub(float e, Z0) { return e; }
 __device__ __forceinline__ float ssub(float e, SV<false> r) { return e - r.v; }
 __device__ __forceinline__ float ssub(float e, SV<true> r) { return e + r.v; }
@@ -1884,8 +1892,15 @@ __device__ __forceinline__ float2 esub2(float2 e, SV<NA> a, SV<NB> b, float2 pm,
 #define ADCT_SWEEP_PAIR 1  // per-block (n, 7 - n) error pairs (esub2) in the scalar-butterfly sweep
 #endif
 
+#ifndef ADCT_SWEEP_SPLIT
+#define ADCT_SWEEP_SPLIT 1  // one block of the lane's pair at a time (fewer live registers)
+#endif
+#ifndef ADCT_SPLIT_UNROLL
+#define ADCT_SPLIT_UNROLL 1
+#endif
+constexpr int kSplitUnroll = ADCT_SPLIT_UNROLL;
 #ifndef ADCT_INC_MINB
-#define ADCT_INC_MINB 2
+#define ADCT_INC_MINB 2  // measured (profiles/r02_variants_sweep_split.txt): 2 > 3 > 4 CTAs/SM
 #endif
 template <int UNUSED = 0>
 __global__ void __launch_bounds__(WARPS * 32, ADCT_INC_MINB)
@@ -1919,6 +1934,57 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INC_MINB)
     uint32_t Y[8][8];
     constexpr bool MIRB = ADCT_MIRB;  // block B column-mirrored (pack_rows_mirb): SSE only, errors mirrored
     compress_fwd<36, MODE_ZONAL, MIRB>(tile, lane, Y);
+    if constexpr (ADCT_SWEEP_SPLIT) {
+      // one block at a time: 36 scalar weighted coefficients live instead of 36 (A, B) pairs, so the
+      // kernel fits 3 CTAs per SM without spills (the packed Y stays live for the second block)
+      float2 acc[NB];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) acc[b] = f2(0.f);
+#pragma unroll (kSplitUnroll)
+      for (int blk = 0; blk < 2; ++blk) {  // a run-time loop (unroll 1): ptxas keeps one block's plane live
+        const uint32_t csel = blk ? 0x7632u : 0x7610u;
+        float VS[64];
+        static_for<64>([&](auto KLc) {
+          constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
+          if constexpr (k + l < NB) {
+            constexpr int c = wclass(k, l);
+            VS[kl] = fmaf(__uint_as_float(__byte_perm(Y[k][l], 0x4B000000u, csel)), p.tab.wc[c], p.tab.cc[c]);
+          }
+        });
+        const bool mir = MIRB && blk;  // block B column-mirrored: output column N is its pixel 7 - N
+        static_for<8>([&](auto Ic) {
+          constexpr int I = decltype(Ic)::value;
+          const uint2 w = lds64_reload(tile + (I + 8 * blk) * TILE_W + lane * 8);
+          auto px576 = [&](auto Nc) {  // 576 x for output column N
+            constexpr int N = decltype(Nc)::value;
+            constexpr uint32_t sel = ((N >> 1) & 1) ? 0x4342u : 0x4140u;
+            constexpr uint32_t selm = ((N >> 1) & 1) ? 0x4041u : 0x4243u;
+            const uint32_t word = ((N < 4) != mir) ? w.x : w.y;
+            return fhfma576<(N & 1) != 0, true>(__byte_perm(word, p.h16magic, mir ? selm : sel), -DC_BIAS16);
+          };
+          float2 e[4];
+          static_for<4>([&](auto Nc) {
+            constexpr int N = decltype(Nc)::value;
+            e[N] = make_float2(px576(cuda::std::integral_constant<int, N>{}),
+                               px576(cuda::std::integral_constant<int, 7 - N>{}));
+          });
+          static_for<NB>([&](auto Bc) {
+            constexpr int B = decltype(Bc)::value;
+            auto rr = inv8s(band_in_v<B, I, 0>(VS), band_in_v<B, I, 1>(VS), band_in_v<B, I, 2>(VS),
+                            band_in_v<B, I, 3>(VS), band_in_v<B, I, 4>(VS), band_in_v<B, I, 5>(VS),
+                            band_in_v<B, I, 6>(VS), band_in_v<B, I, 7>(VS), p.tab.pm1);
+            static_for<4>([&](auto Nc) {
+              constexpr int N = decltype(Nc)::value;
+              e[N] = esub2(e[N], cuda::std::get<N>(rr), cuda::std::get<7 - N>(rr), p.tab.pm1, p.tab.pmr);
+              acc[B] = f2fma(e[N], e[N], acc[B]);
+            });
+          });
+        });
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b) dacc[b] += fx_lane(acc[b], fxs);
+      return;
+    }
     float2 V[64];
     static_for<64>([&](auto KLc) {
       constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
