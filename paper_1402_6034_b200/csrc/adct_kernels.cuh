@@ -708,7 +708,10 @@ __device__ __forceinline__ float2 compress_quant_resid(const uint32_t (&Y)[8][8]
 // large r needs the registers.
 // ------------------------------------------------------------------------------------------
 // measured on B200 (profiles/r01_tune_compress.txt): small r wants occupancy, large r registers
-constexpr int compress_stages(int R) { return (R == 2 || R == 3) ? 3 : 2; }  // r = 2, 3: HBM-side bound
+#ifndef ADCT_ST_ALL
+#define ADCT_ST_ALL 0  // A/B: force one ring depth for every zonal compress kernel
+#endif
+constexpr int compress_stages(int R) { return ADCT_ST_ALL ? ADCT_ST_ALL : (R == 2 || R == 3) ? 3 : 2; }  // r = 2, 3: HBM-side bound
 // residual form from this r on: cheaper once the discarded set is the smaller one;
 // measured with the scalar-butterfly residual (profiles/r02_variants_resid_from.txt): r = 23 residual
 // 0.615 vs direct 0.546 of HBM, r = 22 equal, r <= 21 direct
@@ -746,7 +749,7 @@ constexpr bool compress_grouped(int R) { return !ADCT_NOGROUP && (ADCT_GROUPED |
 #define ADCT_MINB_GRP 4  // grouped mid r (11 <= r < ADCT_RESID_FROM)
 #endif
 #ifndef ADCT_MINB_DS
-#define ADCT_MINB_DS 4  // direct scalar-butterfly form, 4 <= r <= 10
+#define ADCT_MINB_DS 3  // direct form 4 <= r <= 10: 3 CTAs/SM, no spills (r = 6 +1 %, profiles/r02_variants_minb3.txt)
 #endif
 constexpr int compress_minb(int R) {
   // r = 64 (lossless, all 64 coefficients through the direct form): 2 CTAs/SM, no spills (4 spilled 824 B)
