@@ -426,7 +426,44 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
     else if constexpr (RECON != REC_NONE)
       store_recon_row<RECON, (MODE == MODE_ZONAL), (MODE == MODE_ZONAL ? U8_FAST576 : U8_SAFEX)>(rbase, p.recon_pitch, p.h, p.w, ty * TILE_H + I, col, xr);
   };
-  if constexpr (SM == 2 && MODE == MODE_ZONAL && RF < RT && !GROUPED) {
+  if constexpr (SM == 4 && MODE == MODE_ZONAL && RECON == REC_NONE && RF < RT && F16 == 8) {
+    // one block at a time in a run-time loop (half the live floats of the (A, B) forms): per-block
+    // scalar plane, one-instruction butterflies, each pixel's error through FHFMA, squares of the
+    // (n, 7 - n) output pairs of one block
+#pragma unroll 1
+    for (int blk = 0; blk < 2; ++blk) {
+      const uint32_t csel = blk ? 0x7632u : 0x7610u;
+      float2 V1[64];
+      static_for<64>([&](auto KLc) {
+        constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
+        if constexpr (kept(RF, k, l)) {
+          constexpr int c = wclass(k, l);
+          const float cc = kl == 0 ? p.tab.cc[c] + DC_BIAS16 : p.tab.cc[c];
+          V1[kl] = make_float2(fmaf(__uint_as_float(__byte_perm(Y[k][l], 0x4B000000u, csel)), p.tab.wc[c], cc), 0.f);
+        }
+      });
+      const bool mir = MIRB && blk;  // block B column-mirrored: output column N is its pixel 7 - N
+      inverse2d_s1<RF>(V1, p.tab.pm1, [&](auto Ic, const auto& ra) {
+        constexpr int I = decltype(Ic)::value;
+        using cuda::std::get;
+        const uint2 w = lds64_reload(tile + (I + 8 * blk) * TILE_W + lane * 8);
+        auto err = [&](auto Mc) {  // R' - 576 (1024 + x) = R - 576 x for output column M, exact
+          constexpr int M = decltype(Mc)::value;
+          constexpr uint32_t sel = ((M >> 1) & 1) ? 0x4342u : 0x4140u;
+          constexpr uint32_t selm = ((M >> 1) & 1) ? 0x4041u : 0x4243u;
+          const uint32_t h = __byte_perm(((M < 4) != mir) ? w.x : w.y, p.h16magic, mir ? selm : sel);
+          const auto r = get<M>(ra);
+          return fhfma576<(M & 1) != 0, cuda::std::decay_t<decltype(r)>::neg>(h, r.v);
+        };
+        static_for<4>([&](auto Nc) {
+          constexpr int N = decltype(Nc)::value;
+          const float2 e = make_float2(err(cuda::std::integral_constant<int, N>{}),
+                                       err(cuda::std::integral_constant<int, 7 - N>{}));
+          acc[N] = f2fma(e, e, acc[N]);
+        });
+      });
+    }
+  } else if constexpr (SM == 2 && MODE == MODE_ZONAL && RF < RT && !GROUPED) {
     // bank-planned scalar inverse (inv8p) on per-block planes converted as register pairs
     float VS[2][64], UHS[2][8][8];
     convert_planned<RF>(Y, p, F16 > 0 ? DC_BIAS16 : 0.f, VS);
@@ -745,6 +782,15 @@ constexpr bool compress_grouped(int R) { return !ADCT_NOGROUP && (ADCT_GROUPED |
 #ifndef ADCT_MINB_R3
 #define ADCT_MINB_R3 3  // r = 2, 3 (3-stage ring): 4 CTAs/SM spilled (LDL/STL); 3 CTAs: r = 3 0.91 -> 0.96 of HBM (profiles/r02_variants_r3_minb.txt)
 #endif
+#ifndef ADCT_SM4_LO
+#define ADCT_SM4_LO 18  // the per-block run-time loop flavour (SM = 4) for the grouped r in [LO, HI]
+#endif
+#ifndef ADCT_SM4_HI
+#define ADCT_SM4_HI 22  // measured (profiles/r02_variants_sm4.txt): r = 18-22 +1-2 %, r <= 15 slower
+#endif
+#ifndef ADCT_MINB_SM4
+#define ADCT_MINB_SM4 4
+#endif
 #ifndef ADCT_MINB_GRP
 #define ADCT_MINB_GRP 4  // grouped mid r (11 <= r < ADCT_RESID_FROM)
 #endif
@@ -754,7 +800,9 @@ constexpr bool compress_grouped(int R) { return !ADCT_NOGROUP && (ADCT_GROUPED |
 constexpr int compress_minb(int R) {
   // r = 64 (lossless, all 64 coefficients through the direct form): 2 CTAs/SM, no spills (4 spilled 824 B)
   return compress_resid_r(R) ? ADCT_MINB_RESID
-         : (R == 1 ? 6 : (R == 2 || R == 3) ? ADCT_MINB_R3 : R == 64 ? 2 : (R >= 4 && R <= 10) ? ADCT_MINB_DS : compress_grouped(R) ? ADCT_MINB_GRP : 4);
+         : (R == 1 ? 6 : (R == 2 || R == 3) ? ADCT_MINB_R3 : R == 64 ? 2 : (R >= 4 && R <= 10) ? ADCT_MINB_DS
+            : (compress_grouped(R) && R >= ADCT_SM4_LO && R <= ADCT_SM4_HI) ? ADCT_MINB_SM4
+            : compress_grouped(R) ? ADCT_MINB_GRP : 4);
 }
 
 #ifndef ADCT_QUANT_RING_R
@@ -771,17 +819,20 @@ constexpr int compress_minb(int R) {
 #define ADCT_HYB_LO 12
 #endif
 #ifndef ADCT_HYB_HI
-#define ADCT_HYB_HI 18
+#define ADCT_HYB_HI 17
 #endif
 // measured per r (profiles/r02_variants_inverse_flavour*.txt, r02_variants_hybrid_mid_r.txt,
 // r02_variants_low_high_r.txt): scalar butterflies for the ungrouped direct form (r <= 10, except
 // r = 2-4, 7, 8 where f32x2 is 1-4 % faster) and the residual form (r >= 23: +6-9 %), the hybrid
-// (f32x2 columns, scalar rows) for the grouped r = 12..18 (+2-5 %), f32x2 for the other grouped r
-// (r = 20, 21: the hybrid loses 2-4 %) and the quantiser
+// (f32x2 columns, scalar rows) for the grouped r = 12..17 (+2-5 %), the per-block run-time loop
+// (SM = 4: one block's plane live, scalar butterflies) for r = 18..22 (+1-2 %), f32x2 for r = 11 and
+// the quantiser
 constexpr int sinv_mode(int R, int MODE, int RECON) {
   return ADCT_SINV >= 0 ? ADCT_SINV
          : (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT && !compress_grouped(R) &&
             !(R >= 2 && R <= 4) && R != 7 && R != 8)                                               ? 1
+         : (MODE == MODE_ZONAL && RECON == REC_NONE && compress_grouped(R) && R >= ADCT_SM4_LO && R <= ADCT_SM4_HI)
+             ? 4
          : (MODE == MODE_ZONAL && RECON == REC_NONE && compress_grouped(R) && R >= ADCT_HYB_LO && R <= ADCT_HYB_HI)
              ? 3
              : 0;
