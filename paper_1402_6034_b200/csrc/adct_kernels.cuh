@@ -524,7 +524,27 @@ __device__ __forceinline__ float2 compress_resid(const uint32_t (&Y)[8][8], cons
       acc[4 + N] = sq2(get<N>(rb), get<7 - N>(rb), acc[4 + N]);
     });
   };
-  if constexpr (SM == 2 && !GROUPED) {
+  if constexpr (SM == 4 && !GROUPED) {  // one block at a time in a run-time loop (see compress_inv)
+#pragma unroll 1
+    for (int blk = 0; blk < 2; ++blk) {
+      const uint32_t csel = blk ? 0x7632u : 0x7610u;
+      float2 V1[64];
+      static_for<64>([&](auto KLc) {
+        constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
+        if constexpr (kept(RM, k, l)) {
+          constexpr int c = wclass(k, l);
+          V1[kl] = make_float2(fmaf(__uint_as_float(__byte_perm(Y[k][l], 0x4B000000u, csel)), p.tab.wc[c], p.tab.cc[c]), 0.f);
+        }
+      });
+      inverse2d_s1<RM>(V1, p.tab.pm1, [&](auto Ic, const auto& ra) {
+        using cuda::std::get;
+        static_for<4>([&](auto Nc) {
+          constexpr int N = decltype(Nc)::value;
+          acc[N] = sq2(get<N>(ra), get<7 - N>(ra), acc[N]);
+        });
+      });
+    }
+  } else if constexpr (SM == 2 && !GROUPED) {
     float VS[2][64], UHS[2][8][8];
     convert_planned<RM>(Y, p, 0.f, VS);
     inverse2d_p<RM>(VS, UHS, p.tab.pm1, p.tab.pmr, sq_row_s);
@@ -788,6 +808,13 @@ constexpr bool compress_grouped(int R) { return !ADCT_NOGROUP && (ADCT_GROUPED |
 #ifndef ADCT_SM4_HI
 #define ADCT_SM4_HI 22  // measured (profiles/r02_variants_sm4.txt): r = 18-22 +1-2 %, r <= 15 slower
 #endif
+#ifndef ADCT_RSM4_LO
+#define ADCT_RSM4_LO 99  // the per-block loop for the residual form (no injected columns) in [LO, HI]:
+                          // measured 5-9 % slower at r = 29..50 (profiles/r02_variants_sm4.txt), off
+#endif
+#ifndef ADCT_RSM4_HI
+#define ADCT_RSM4_HI 0
+#endif
 #ifndef ADCT_MINB_SM4
 #define ADCT_MINB_SM4 4
 #endif
@@ -829,6 +856,8 @@ constexpr int compress_minb(int R) {
 // the quantiser
 constexpr int sinv_mode(int R, int MODE, int RECON) {
   return ADCT_SINV >= 0 ? ADCT_SINV
+         : (MODE == MODE_ZONAL && RECON == REC_NONE && compress_resid_r(R) && hcol_mask(R) == 0 &&
+            R >= ADCT_RSM4_LO && R <= ADCT_RSM4_HI)                                                ? 4
          : (MODE == MODE_ZONAL && RECON == REC_NONE && R < RT && !compress_grouped(R) &&
             !(R >= 2 && R <= 4) && R != 7 && R != 8)                                               ? 1
          : (MODE == MODE_ZONAL && RECON == REC_NONE && compress_grouped(R) && R >= ADCT_SM4_LO && R <= ADCT_SM4_HI)
