@@ -55,19 +55,40 @@ def analyse(objs, only=None, mode=0, recon=0):
             r = int(m.group(1))
             if only and r not in only:
                 continue
-            ops = []
-            for line in blk.split("\n"):
-                mm = LINE.match(line)
-                if mm:
-                    ops.append((mm.group(2), mm.group(3)))
-            names = [op.split(".")[0] for op, _ in ops]
-            body = [i for i, op in enumerate(names) if op in ("LDS", "FFMA2", "FADD2")]
-            waits = [i for i, op in enumerate(names) if op == "SYNCS" and i > body[0]]
-            seg = ops[body[0]:waits[0]] if waits else ops[body[0]:body[-1]]
-            cyc = sum(instr_cost(op, a) for op, a in seg)
+            n, cyc = tile_body_cost(blk)
             if r not in res or cyc < res[r][1]:  # several instantiations (e.g. QLO): the lightest
-                res[r] = (len(seg), cyc)
+                res[r] = (n, cyc)
     return res
+
+
+ADDR = re.compile(r"\s+/\*([0-9a-f]{4,})\*/")
+
+
+def tile_body_cost(blk, loop_trips=2):
+    """(instructions, read cycles) of one tile body: from the first shared-memory load after the
+    ring's first mbarrier wait (SYNCS.PHASECHK) to the next SYNCS; a backward branch inside it (the
+    per-block run-time loop of the SM = 4 flavour) counts its loop body loop_trips times."""
+    ops = []
+    for line in blk.split("\n"):
+        mm = LINE.match(line)
+        if mm:
+            ops.append((int(ADDR.match(line).group(1), 16), mm.group(2), mm.group(3)))
+    chk = [i for i, (_, op, _) in enumerate(ops) if op.startswith("SYNCS.PHASECHK")]
+    first = chk[0] if chk else 0
+    start = next(i for i in range(first, len(ops)) if ops[i][1].startswith("LDS"))
+    end = next((i for i in range(start + 1, len(ops)) if ops[i][1].startswith("SYNCS")), len(ops))
+    seg = ops[start:end]
+    n = len(seg)
+    cyc = sum(instr_cost(op, a) for _, op, a in seg)
+    for k, (addr, op, a) in enumerate(seg):
+        if op.startswith("BRA"):
+            m = re.search(r"0x([0-9a-f]+)", a)
+            tgt = int(m.group(1), 16) if m else None
+            if tgt is not None and seg[0][0] <= tgt < addr:
+                loop = [x for x in seg if tgt <= x[0] <= addr]
+                n += (loop_trips - 1) * len(loop)
+                cyc += (loop_trips - 1) * sum(instr_cost(op2, a2) for _, op2, a2 in loop)
+    return n, cyc
 
 
 def write_json(path):
