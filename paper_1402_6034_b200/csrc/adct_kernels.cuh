@@ -803,10 +803,10 @@ constexpr bool compress_grouped(int R) { return !ADCT_NOGROUP && (ADCT_GROUPED |
 #define ADCT_MINB_R3 3  // r = 2, 3 (3-stage ring): 4 CTAs/SM spilled (LDL/STL); 3 CTAs: r = 3 0.91 -> 0.96 of HBM (profiles/r02_variants_r3_minb.txt)
 #endif
 #ifndef ADCT_SM4_LO
-#define ADCT_SM4_LO 18  // the per-block run-time loop flavour (SM = 4) for the grouped r in [LO, HI]
+#define ADCT_SM4_LO 15  // the per-block run-time loop flavour (SM = 4) for the grouped r in [LO, HI]
 #endif
 #ifndef ADCT_SM4_HI
-#define ADCT_SM4_HI 22  // measured (profiles/r02_variants_sm4.txt): r = 18-22 +1-2 %, r <= 15 slower
+#define ADCT_SM4_HI 22  // measured (profiles/r02_variants_sm4.txt): r = 15-22 +1-3 %, r <= 14 slower
 #endif
 #ifndef ADCT_RSM4_LO
 #define ADCT_RSM4_LO 99  // the per-block loop for the residual form (no injected columns) in [LO, HI]:
@@ -846,13 +846,13 @@ constexpr int compress_minb(int R) {
 #define ADCT_HYB_LO 12
 #endif
 #ifndef ADCT_HYB_HI
-#define ADCT_HYB_HI 17
+#define ADCT_HYB_HI 14
 #endif
 // measured per r (profiles/r02_variants_inverse_flavour*.txt, r02_variants_hybrid_mid_r.txt,
 // r02_variants_low_high_r.txt): scalar butterflies for the ungrouped direct form (r <= 10, except
 // r = 2-4, 7, 8 where f32x2 is 1-4 % faster) and the residual form (r >= 23: +6-9 %), the hybrid
-// (f32x2 columns, scalar rows) for the grouped r = 12..17 (+2-5 %), the per-block run-time loop
-// (SM = 4: one block's plane live, scalar butterflies) for r = 18..22 (+1-2 %), f32x2 for r = 11 and
+// (f32x2 columns, scalar rows) for the grouped r = 12..14 (+2-5 %), the per-block run-time loop
+// (SM = 4: one block's plane live, scalar butterflies) for r = 15..22 (+1-3 %), f32x2 for r = 11 and
 // the quantiser
 constexpr int sinv_mode(int R, int MODE, int RECON) {
   return ADCT_SINV >= 0 ? ADCT_SINV
