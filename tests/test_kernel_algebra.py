@@ -47,19 +47,23 @@ def _forms(out):
     return A, c
 
 
+@pytest.mark.parametrize("graph", list(EB.GRAPHS))
 @pytest.mark.parametrize("r", list(range(1, 65)))
-def test_direct_graph_is_R(r):
+def test_direct_graph_is_R(r, graph):
+    """Every inverse flavour the kernels use (f32x2 inv8, one-instruction-butterfly inv8s, and the
+    hybrid of the two) computes exactly T^T (W . M_r . Y) T (+ the DC bias) with every node < 2^24."""
     for bias in EB.DC_BIASES:
-        m, out = EB.run(r, "direct", bias)
+        m, out = EB.run(r, "direct", bias, graph)
         A, c = _forms(out)
         assert np.array_equal(A, _affine_R(r))
         assert np.all(c == bias)
         assert m < 2 ** 24
 
 
+@pytest.mark.parametrize("graph", list(EB.GRAPHS))
 @pytest.mark.parametrize("r", list(range(1, 64)))
-def test_residual_graph_is_error(r):
-    m, out = EB.run(r, "residual")
+def test_residual_graph_is_error(r, graph):
+    m, out = EB.run(r, "residual", 0, graph)
     A, c = _forms(out)
     assert np.array_equal(A, 576 * np.eye(64, dtype=np.int64) - _affine_R(r))
     assert np.all(c == 0)

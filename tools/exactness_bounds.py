@@ -85,6 +85,23 @@ def inv8(B, x):
             sub(B, a3, b3), sub(B, a2, b2), sub(B, a1, b1), sub(B, a0, b0)]
 
 
+def inv8s(B, x):
+    """The one-instruction-butterfly graph (adct_device.cuh inv8s): the same outputs through the
+    intermediate nodes x1 +- x3 and x5 +- x7 instead of inv8's (x1 + x3), (x1 - x5), (x1 - x3), (x5 - x3)."""
+    p, q = add(B, x[0], x[4]), sub(B, x[0], x[4])
+    a0, a3 = add(B, p, x[2]), sub(B, p, x[2])
+    a2, a1 = add(B, q, x[6]), sub(B, q, x[6])
+    s13p, s13m = add(B, x[1], x[3]), sub(B, x[1], x[3])
+    s57p, s57m = add(B, x[5], x[7]), sub(B, x[5], x[7])
+    b0, b1 = add(B, s13p, x[5]), sub(B, x[1], s57p)
+    b2, b3 = add(B, s13m, x[7]), sub(B, s57m, x[3])
+    return [add(B, a0, b0), add(B, a1, b1), add(B, a2, b2), add(B, a3, b3),
+            sub(B, a3, b3), sub(B, a2, b2), sub(B, a1, b1), sub(B, a0, b0)]
+
+
+GRAPHS = {"f32x2": (inv8, inv8), "scalar": (inv8s, inv8s), "hybrid": (inv8, inv8s)}  # (columns, rows)
+
+
 def forms_Y():
     """Y_kl = sum_ij T_ki T_lj x_ij as affine forms (64 coefficients + constant)."""
     Y = np.zeros((8, 8, 65), dtype=np.int64)
@@ -94,7 +111,7 @@ def forms_Y():
     return Y
 
 
-def run(r: int, variant: str, bias: int = 0):
+def run(r: int, variant: str, bias: int = 0, graph: str = "f32x2"):
     B = Bound()
     Y = forms_Y()
     V = [[None] * 8 for _ in range(8)]
@@ -108,8 +125,9 @@ def run(r: int, variant: str, bias: int = 0):
         V[0][0] = V[0][0].copy()
         V[0][0][64] += bias
         B.see(V[0][0])
-    U = [inv8(B, [V[k][l] for k in range(8)]) for l in range(8)]
-    out = [inv8(B, [U[l][i] for l in range(8)]) for i in range(8)]
+    col, row = GRAPHS[graph]
+    U = [col(B, [V[k][l] for k in range(8)]) for l in range(8)]
+    out = [row(B, [U[l][i] for l in range(8)]) for i in range(8)]
     # check the final identity: direct -> R + bias, residual -> 576 x - R
     return B.max, out
 
@@ -146,15 +164,16 @@ def run_band_chain():
 
 def main():
     worst = 0
-    for variant, bias in (("direct", 0), ("direct", DC_BIASES[1]), ("direct", DC_BIASES[2]), ("residual", 0)):
-        row = []
-        for r in range(1, 65):
-            if variant == "residual" and r == 64:
-                continue
-            m, _ = run(r, variant, bias)
-            worst = max(worst, m)
-            row.append(f"{r}:{m}")
-        print(variant, f"bias={bias}", " ".join(row))
+    for graph in GRAPHS:  # the kernels' three inverse flavours (sinv_mode)
+        for variant, bias in (("direct", 0), ("direct", DC_BIASES[1]), ("direct", DC_BIASES[2]), ("residual", 0)):
+            row = []
+            for r in range(1, 65):
+                if variant == "residual" and r == 64:
+                    continue
+                m, _ = run(r, variant, bias, graph)
+                worst = max(worst, m)
+                row.append(f"{r}:{m}")
+            print(graph, variant, f"bias={bias}", " ".join(row))
     m, _ = run_band_chain()
     worst = max(worst, m)
     print("band chain (k_compress_sweep_inc)", m)
