@@ -79,9 +79,10 @@ def test_exactness_tool_exit_code():
     assert EB.main() == 0
 
 
-def test_band_chain_equals_error_per_r():
+@pytest.mark.parametrize("row_graph", ["inv8", "inv8s"])
+def test_band_chain_equals_error_per_r(row_graph):
     # k_compress_sweep_inc: after band b the running per-pixel form is 576 x - R_r, r = (b+1)(b+2)/2
-    m, finals = EB.run_band_chain()
+    m, finals = EB.run_band_chain(getattr(EB, row_graph))
     assert m < 2 ** 24
     for r, e in finals.items():
         A_, c = _forms(e)
