@@ -779,7 +779,10 @@ constexpr int compress_resid_r(int R) { return R >= ADCT_RESID_FROM && R < 64; }
 // output rows per tile that take the f16 error route (ALU -> FMA pipe rebalancing, compress_inv)
 // measured on B200 (profiles/r01_tune_fhfma.txt): the FHFMA error route wins for every direct r
 // (r = 1 keeps two rows on the f32 route to balance its ALU-light body)
-constexpr int compress_f16_rows(int R) { return R == 1 ? 6 : 8; }
+#ifndef ADCT_F16_R1
+#define ADCT_F16_R1 6
+#endif
+constexpr int compress_f16_rows(int R) { return R == 1 ? ADCT_F16_R1 : 8; }
 // inverse output rows in two register-light groups (inverse2d_grouped)
 #ifndef ADCT_GROUPED
 #define ADCT_GROUPED 0
