@@ -399,7 +399,7 @@ __device__ __forceinline__ float2 compress_inv(const uint32_t (&Y)[8][8], const 
     using cuda::std::get;
     const uint2 wa = lds64_reload(tile + I * TILE_W + lane * 8);
     const uint2 wb = lds64_reload(tile + (I + 8) * TILE_W + lane * 8);
-    float2 xr[8];
+    [[maybe_unused]] float2 xr[8];  // reconstruction row (RECON kernels only)
     static_for<8>([&](auto Nc) {
       constexpr int N = decltype(Nc)::value;
       if constexpr (I < F16) {
