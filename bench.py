@@ -294,10 +294,17 @@ def main():
     from synth import images as S
 
     A.load()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # functional check of the multi-rank path on a one-GPU box (NOT a measurement): every rank on
+    # cuda:0 with gloo collectives (ranks never wait on each other's kernels, only on the all-reduce)
+    one_dev = os.environ.get("ADCT_BENCH_ONE_DEVICE") == "1"
+    local_dev = 0 if one_dev else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     n_total = a.images if a.scaling == "strong" else a.images * world
     lo, hi = shard_range(n_total, rank, world)
     n_loc = hi - lo
@@ -329,7 +336,7 @@ def main():
             for _ in R_SET] for _ in range(a.steps)]
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = A.launch_count()
-    with ClockSampler(local) as clk:
+    with ClockSampler(local_dev) as clk:
         torch.cuda.synchronize()
         t_start.record(stream)
         for s in range(a.steps):
