@@ -230,8 +230,11 @@ def test_compress_recon_f32_and_u8(r):
 @pytest.mark.parametrize("h,w", [(8, 8), (8, 16), (24, 504), (40, 264), (264, 8), (16, 520),
                                  (8, 131080), (65544, 8)])
 def test_compress_ragged_shapes(h, w):
+    """Ragged geometries through one r of every kernel form and inverse flavour (sinv_mode): scalar
+    direct (1, 10), f32x2 direct (3), grouped f32x2 (11), hybrid (13), per-block loop (15, 21),
+    residual with an injected column (23, 28), residual (36), lossless (64)."""
     imgs = rng.integers(0, 256, (5, h, w), dtype=np.uint8)
-    for r in (1, 10, 36, 64):
+    for r in (1, 3, 10, 11, 13, 15, 21, 23, 28, 36, 64):
         sse = host(A.compress_psnr(dev(imgs), r))
         want = O.compress_zonal_sse(imgs, r)
         if r == 64:
