@@ -332,6 +332,10 @@ adct_status compress_dispatch(const CUtensorMap& map, const CUtensorMap& omap, b
   if (recon_t == ADCT_RECON_NONE) {
     return launch_compress(zonal_kernel(r), r, map, p, s);
   }
+  if (bulk) {  // C5's r: compile-time mask (pruned forward / inverse); any other r: the runtime mask
+    const int rt = recon_t == ADCT_RECON_F32 ? REC_F32 : REC_U8;
+    if (ReconKernel k = zonal_recon_kernel(r, rt)) return launch_tma2(k, map, omap, p, crec_smem_bytes(rt), s);
+  }
   if (bulk && recon_t == ADCT_RECON_F32)
     return launch_tma2(k_compress_recon<MODE_ZONAL, REC_F32>, map, omap, p, crec_smem_bytes(REC_F32), s);
   if (bulk) return launch_tma2(k_compress_recon<MODE_ZONAL, REC_U8>, map, omap, p, crec_smem_bytes(REC_U8), s);

@@ -1451,10 +1451,13 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INVT_MINB)
 constexpr int crec_smem_bytes(int RECON) {
   return WARPS * 2 * TILE_BYTES + FWDT_BAR_BYTES + WARPS * recon_stage_bytes(RECON);
 }
-template <int MODE, int RECON>
+// R = RT: the runtime mask (any r, and the quantiser); R < RT: a compile-time zonal mask (C5's r set,
+// recon_parts.cu) — the forward and the inverse pruned to the kept coefficients
+template <int MODE, int RECON, int R = RT>
 __global__ void __launch_bounds__(WARPS * 32, ADCT_MINB_RT)
     k_compress_recon(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap omap,
                      const __grid_constant__ CompressParams p) {
+  static_assert(R == RT || MODE == MODE_ZONAL, "compile-time masks: zonal only");
   constexpr int ST = 2;
   extern __shared__ __align__(128) uint8_t smem[];
   const double kSseScale = (MODE == MODE_ZONAL) ? 1.0 / 331776.0 : 1.0;
@@ -1475,10 +1478,10 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_MINB_RT)
       acc = 0;
     }
     uint32_t Y[8][8];
-    compress_fwd<RT, MODE>(tile, lane, Y);
+    compress_fwd<R, MODE>(tile, lane, Y);
     if (lane == 0) bulk_wait_read<0>();  // the previous tile's store has finished reading `buf`
     __syncwarp();
-    const float2 e2 = compress_inv<RT, MODE, RECON, 0, false, true>(Y, tile, lane, p, img, ty, tx, buf);
+    const float2 e2 = compress_inv<R, MODE, RECON, 0, false, true>(Y, tile, lane, p, img, ty, tx, buf);
     acc += fx_lane(e2, fxs);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
@@ -2359,6 +2362,8 @@ template <bool LO> constexpr CompressKernel quant64_kernel() {
                      (bool)ADCT_MIRB, LO, sinv_mode(64, MODE_QUANT, REC_NONE)>;
 }
 CompressKernel multi_kernel_c5();  // k_compress_multi<RSetC5>, instantiated in multi_r.cu
+typedef void (*ReconKernel)(CUtensorMap, CUtensorMap, CompressParams);
+ReconKernel zonal_recon_kernel(int r, int recon);  // compile-time-r reconstruction kernels (recon_parts.cu)
 CompressKernel sweep_inc_kernel_c5();  // k_compress_sweep_inc, instantiated in multi_r.cu
 // zonal kernels k_compress<r, ZONAL, RECON_NONE>, instantiated in zonal_part*.cu (4 TUs)
 CompressKernel zonal_kernel(int r);

@@ -699,7 +699,8 @@ def test_no_writes_outside_outputs(n, h, w):
         A.compress_psnr(x, r, q=q, sse=sse_big[:n])
         assert torch.all(sse_big[n:] == canary_f)
     for kind, dt, fill in [("f32", torch.float32, canary_f), ("u8", torch.uint8, canary_u)]:
-        for r, q in [(10, 0.0), (36, 0.0), (64, 16.0)]:
+        # 10, 36: compile-time-r kernels (recon_parts.cu); 20: the runtime mask; 64 q16: the quantiser
+        for r, q in [(10, 0.0), (36, 0.0), (20, 0.0), (64, 16.0)]:
             big, win = _window(n, h, w, dt, fill)
             A.compress_psnr(x, r, q=q, recon=kind, recon_out=win)
             assert torch.all(_outside(big, n, h, w) == fill), (kind, r, q)
@@ -717,6 +718,8 @@ def test_no_writes_outside_outputs(n, h, w):
     assert torch.all(_outside(big, n, h, w) == canary_f)
     e_big = torch.full((n + 2, 16), canary_i, dtype=torch.int64, device="cuda")
     A.diag_energy(x, energy=e_big[:n])
+    assert torch.all(e_big[n:] == canary_i)
+    A.diag_energy(x, energy=e_big[:n], r_max=36)
     assert torch.all(e_big[n:] == canary_i)
     u_big = torch.full((n + 4,), canary_f, dtype=torch.float64, device="cuda")
     A.uqi(x, A.compress_psnr(x, 10, recon="f32")[1], out=u_big[:n])
