@@ -1451,6 +1451,9 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_INVT_MINB)
 constexpr int crec_smem_bytes(int RECON) {
   return WARPS * 2 * TILE_BYTES + FWDT_BAR_BYTES + WARPS * recon_stage_bytes(RECON);
 }
+#ifndef ADCT_RECON_SM
+#define ADCT_RECON_SM 0  // inverse flavour of the compile-time-r reconstruction kernels (A/B knob)
+#endif
 // R = RT: the runtime mask (any r, and the quantiser); R < RT: a compile-time zonal mask (C5's r set,
 // recon_parts.cu) — the forward and the inverse pruned to the kept coefficients
 template <int MODE, int RECON, int R = RT>
@@ -1481,7 +1484,8 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_MINB_RT)
     compress_fwd<R, MODE>(tile, lane, Y);
     if (lane == 0) bulk_wait_read<0>();  // the previous tile's store has finished reading `buf`
     __syncwarp();
-    const float2 e2 = compress_inv<R, MODE, RECON, 0, false, true>(Y, tile, lane, p, img, ty, tx, buf);
+    const float2 e2 = compress_inv<R, MODE, RECON, 0, false, true, false, (R < RT ? ADCT_RECON_SM : 0)>(
+        Y, tile, lane, p, img, ty, tx, buf);
     acc += fx_lane(e2, fxs);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
