@@ -768,7 +768,15 @@ __device__ __forceinline__ float2 compress_quant_resid(const uint32_t (&Y)[8][8]
 #ifndef ADCT_ST_ALL
 #define ADCT_ST_ALL 0  // A/B: force one ring depth for every zonal compress kernel
 #endif
-constexpr int compress_stages(int R) { return ADCT_ST_ALL ? ADCT_ST_ALL : (R == 2 || R == 3) ? 3 : 2; }  // r = 2, 3: HBM-side bound
+#ifndef ADCT_R1_ST
+#define ADCT_R1_ST 3  // r = 1: 3-stage ring at 4 CTAs/SM, +1.4 % interleaved (profiles/r02_variants_r1_ring.txt)
+#endif
+#ifndef ADCT_R1_MINB
+#define ADCT_R1_MINB 4
+#endif
+constexpr int compress_stages(int R) {
+  return ADCT_ST_ALL ? ADCT_ST_ALL : R == 1 ? ADCT_R1_ST : (R == 2 || R == 3) ? 3 : 2;  // r = 2, 3: HBM-side bound
+}
 // residual form from this r on: cheaper once the discarded set is the smaller one;
 // measured with the scalar-butterfly residual (profiles/r02_variants_resid_from.txt): r = 23 residual
 // 0.615 vs direct 0.546 of HBM, r = 22 equal, r <= 21 direct
@@ -830,7 +838,7 @@ constexpr bool compress_grouped(int R) { return !ADCT_NOGROUP && (ADCT_GROUPED |
 constexpr int compress_minb(int R) {
   // r = 64 (lossless, all 64 coefficients through the direct form): 2 CTAs/SM, no spills (4 spilled 824 B)
   return compress_resid_r(R) ? ADCT_MINB_RESID
-         : (R == 1 ? 6 : (R == 2 || R == 3) ? ADCT_MINB_R3 : R == 64 ? 2 : (R >= 4 && R <= 10) ? ADCT_MINB_DS
+         : (R == 1 ? ADCT_R1_MINB : (R == 2 || R == 3) ? ADCT_MINB_R3 : R == 64 ? 2 : (R >= 4 && R <= 10) ? ADCT_MINB_DS
             : (compress_grouped(R) && R >= ADCT_SM4_LO && R <= ADCT_SM4_HI) ? ADCT_MINB_SM4
             : compress_grouped(R) ? ADCT_MINB_GRP : 4);
 }
