@@ -771,11 +771,14 @@ __device__ __forceinline__ float2 compress_quant_resid(const uint32_t (&Y)[8][8]
 #ifndef ADCT_R1_ST
 #define ADCT_R1_ST 3  // r = 1: 3-stage ring at 4 CTAs/SM, +1.4 % interleaved (profiles/r02_variants_r1_ring.txt)
 #endif
+#ifndef ADCT_R3_ST
+#define ADCT_R3_ST 3
+#endif
 #ifndef ADCT_R1_MINB
 #define ADCT_R1_MINB 4
 #endif
 constexpr int compress_stages(int R) {
-  return ADCT_ST_ALL ? ADCT_ST_ALL : R == 1 ? ADCT_R1_ST : (R == 2 || R == 3) ? 3 : 2;  // r = 2, 3: HBM-side bound
+  return ADCT_ST_ALL ? ADCT_ST_ALL : R == 1 ? ADCT_R1_ST : (R == 2 || R == 3) ? ADCT_R3_ST : 2;  // r = 2, 3: HBM-side bound
 }
 // residual form from this r on: cheaper once the discarded set is the smaller one;
 // measured with the scalar-butterfly residual (profiles/r02_variants_resid_from.txt): r = 23 residual
