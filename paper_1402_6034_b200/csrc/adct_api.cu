@@ -576,7 +576,8 @@ adct_status adct_compress_sse576(const uint8_t* src, int64_t n, int64_t h, int64
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMemsetAsync(sse576, 0, sizeof(uint64_t) * (size_t)n, s);
   if (e != cudaSuccess) return cuda_fail(e);
-  if ((st = launch_compress(k_compress_exact<2>, RT, map, p, s))) return st;
+  CompressKernel ek = exact_kernel(r);  // C5's r: compile-time mask; other r: the runtime mask
+  if ((st = launch_compress(ek ? ek : &k_compress_exact<2>, RT, map, p, s))) return st;
   if (!sse) return ADCT_OK;
   const int64_t blocks = (n + 255) / 256;
   k_sse576_to_f64<0><<<(unsigned)(blocks < 1024 ? blocks : 1024), 256, 0, s>>>(p.sse576, sse, n);

@@ -961,12 +961,20 @@ __device__ __forceinline__ unsigned long long sq_exact(float e) {
   const int ei = __float_as_int(e + 12582912.0f) - 0x4B400000;
   return (unsigned long long)((long long)ei * (long long)ei);
 }
+// R = RT: the runtime mask (per-position weights, any r); R < RT: a compile-time mask (C5's r set,
+// exact_parts.cu), per-class weights and the inverse pruned to the kept coefficients
+template <int R = RT>
 __device__ __forceinline__ unsigned long long compress_inv_exact(const uint32_t (&Y)[8][8], const uint8_t* tile,
                                                                  int lane, const CompressParams& p) {
   float2 V[64];
   static_for<64>([&](auto KLc) {
     constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
-    V[kl] = f2fma(biased_pair(Y[k][l]), f2(p.tab.w[kl].x), f2(p.tab.c[kl].x));  // W . M . Y, exact
+    if constexpr (R == RT) {
+      V[kl] = f2fma(biased_pair(Y[k][l]), f2(p.tab.w[kl].x), f2(p.tab.c[kl].x));  // W . M . Y, exact
+    } else if constexpr (kept(R, k, l)) {
+      constexpr int c = wclass(k, l);
+      V[kl] = f2fma(biased_pair(Y[k][l]), f2(p.tab.wc[c]), f2(p.tab.cc[c]));  // W . Y (kept), exact
+    }
   });
   unsigned long long acc = 0ull;
 #if ADCT_EXACT_BITS
@@ -1009,9 +1017,9 @@ __device__ __forceinline__ unsigned long long compress_inv_exact(const uint32_t 
   if constexpr (ADCT_EXACT_SINV) {  // per-block one-instruction butterflies (§7)
     auto err_row_s = [&](auto Ic, const auto& ra, const auto& rb) { err_row(Ic, join_rows(ra, rb)); };
     float2 UH[8][8];  // unused
-    inverse2d_s<RT>(V, UH, p.tab.pm1, err_row_s);
+    inverse2d_s<R>(V, UH, p.tab.pm1, err_row_s);
   } else {
-    inverse2d<RT>(V, err_row);
+    inverse2d<R>(V, err_row);
   }
   auto fold = [](unsigned long long b2, uint32_t s1, int n, uint32_t K) {
     const long long se = (long long)(int32_t)((uint32_t)n * K - s1);  // sum e (sign immaterial)
@@ -1041,7 +1049,7 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-template <int ST>
+template <int ST, int R = RT>
 __global__ void __launch_bounds__(WARPS * 32, ADCT_MINB_RT)
     k_compress_exact(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CompressParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -1060,8 +1068,8 @@ __global__ void __launch_bounds__(WARPS * 32, ADCT_MINB_RT)
       acc = 0ull;
     }
     uint32_t Y[8][8];
-    compress_fwd<RT, MODE_ZONAL>(tile, lane, Y);
-    acc += compress_inv_exact(Y, tile, lane, p);
+    compress_fwd<R, MODE_ZONAL>(tile, lane, Y);
+    acc += compress_inv_exact<R>(Y, tile, lane, p);
   });
   const unsigned long long v = warp_sum_u64(acc);
   if (lane == 0 && cur >= 0) atomicAdd(p.sse576 + cur, v);
@@ -2378,6 +2386,7 @@ template <bool LO> constexpr CompressKernel quant64_kernel() {
 }
 CompressKernel multi_kernel_c5();  // k_compress_multi<RSetC5>, instantiated in multi_r.cu
 typedef void (*ReconKernel)(CUtensorMap, CUtensorMap, CompressParams);
+CompressKernel exact_kernel(int r);  // compile-time-r exact-SSE kernels for C5's r set (exact_parts.cu)
 ReconKernel zonal_recon_kernel(int r, int recon);  // compile-time-r reconstruction kernels (recon_parts.cu)
 CompressKernel sweep_inc_kernel_c5();  // k_compress_sweep_inc, instantiated in multi_r.cu
 // zonal kernels k_compress<r, ZONAL, RECON_NONE>, instantiated in zonal_part*.cu (4 TUs)
