@@ -570,10 +570,15 @@ __device__ __forceinline__ float2 compress_resid(const uint32_t (&Y)[8][8], cons
 #ifndef ADCT_RESID_HC
 #define ADCT_RESID_HC 1
 #endif
+#ifndef ADCT_RESID_PC
+#define ADCT_RESID_PC 1  // also inject the columns whose only kept coefficient is (0, L) (pcol_mask)
+#endif
 template <int R, int SM = 0>
 __device__ __forceinline__ float2 compress_resid_hc(const uint32_t (&Y)[8][8], const uint32_t (&H)[8][8],
                                                     const CompressParams& p) {
-  constexpr int RM = RESID + R, HC = hcol_mask(R);
+  constexpr int PC = ADCT_RESID_PC ? pcol_mask(R) : 0;
+  constexpr int RM = RESID + R, HC = hcol_mask(R) | PC;  // every injected column
+  static_assert(PC == 0 || SM != 2, "the bank-planned flavour injects only fully discarded columns");
   float2 V[64];
   static_for<64>([&](auto KLc) {
     constexpr int kl = decltype(KLc)::value, k = kl / 8, l = kl % 8;
@@ -585,7 +590,18 @@ __device__ __forceinline__ float2 compress_resid_hc(const uint32_t (&Y)[8][8], c
   float2 UH[8][8];
   static_for<8>([&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
-    if constexpr ((HC >> L) & 1) {
+    if constexpr ((PC >> L) & 1) {
+      // only (0, L) kept: the discarded rows' column inverse is (576 / d_L) H[:, L] - W_0L Y_0L =
+      // (W_0L) (8 H[i][L] - Y_0L) with W_0L = 576 / (8 d_L) an integer and Y_0L = sum_i H[i][L]:
+      // 8 H - Y_0L is an exact int16 SWAR lane (|.| <= 32640), one LEA per row, then the same
+      // magic-exponent conversion as a fully injected column
+      const uint32_t y0 = ((H[0][L] + H[1][L]) + (H[2][L] + H[3][L])) + ((H[4][L] + H[5][L]) + (H[6][L] + H[7][L]));
+      const uint32_t off = BIAS2 - y0;
+      constexpr float w0 = (float)(576 / (8 * dval(L)));
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        UH[L][i] = f2fma(biased_pair((H[i][L] << 3) + off), f2(w0), f2(-KF * w0));
+    } else if constexpr ((HC >> L) & 1) {
       constexpr float wl = (float)(576 / dval(L));
 #pragma unroll
       for (int i = 0; i < 8; ++i)  // + 0x80008000: both 16-bit lanes biased (the low lane's borrow cancels)
@@ -913,9 +929,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     uint32_t Y[8][8];
     float2 e2;
     if constexpr (RES) {
-      if constexpr (ADCT_RESID_HC && hcol_mask(R) != 0 && !GRP) {
+      if constexpr (ADCT_RESID_HC && (hcol_mask(R) | (ADCT_RESID_PC ? pcol_mask(R) : 0)) != 0 && !GRP) {
         uint32_t H[8][8];
-        compress_fwd_h<RESID + R, hcol_mask(R), MIRB>(tile, lane, Y, H);
+        compress_fwd_h<RESID + R, hcol_mask(R) | (ADCT_RESID_PC ? pcol_mask(R) : 0), MIRB>(tile, lane, Y, H);
         e2 = compress_resid_hc<R, SM>(Y, H, p);
       } else {
         compress_fwd<RESID + R, MODE, MIRB>(tile, lane, Y);

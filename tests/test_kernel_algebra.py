@@ -100,6 +100,34 @@ def test_fully_discarded_column_identity(L):
     assert 576 % d[L] == 0
 
 
+@pytest.mark.parametrize("L", list(range(1, 8)))
+def test_row0_only_column_identity(L):
+    """compress_resid_hc's partial injection (pcol_mask): for a column L >= 1 whose only kept
+    coefficient is (0, L), the column inverse of the discarded rows 1..7 equals
+    (576 / d_L) H - W_0L (sum_i H_i) 1 = W_0L (8 H - (sum_i H_i) 1), with W_0L = 576 / (8 d_L) an
+    integer, and 8 H_i - sum_j H_j stays inside int16 for every uint8 row-pass column."""
+    T, W = EB.T, EB.W
+    d = np.diag(T @ T.T)
+    D1 = np.diag(W[:, L] * (np.arange(8) != 0))           # discarded rows 1..7 of column L
+    lhs = T.T @ D1 @ T
+    rhs = (576 // d[L]) * np.eye(8, dtype=np.int64) - W[0, L] * np.ones((8, 8), dtype=np.int64)
+    assert np.array_equal(lhs, rhs)
+    assert W[0, L] * 8 == 576 // d[L]
+    # H[:, L] = (X T^T)[:, L] = X T[L]: |8 H_i - sum_j H_j| <= 14 max|H| over uint8 rows
+    assert 14 * (255 * max(T[L][T[L] > 0].sum(), -T[L][T[L] < 0].sum())) < 2 ** 15
+
+
+@pytest.mark.parametrize("r", list(range(23, 64)))
+def test_pcol_columns_are_the_row0_only_ones(r):
+    M = np.array([[EB.zz(i, j) < r for j in range(8)] for i in range(8)])
+    want = [L for L in range(1, 8) if M[0, L] and not M[1:, L].any()]
+    # triangular r = (s+1)(s+2)/2 leave column s with (0, s) alone: r = 28 -> 6, r = 36 -> 7
+    if r == 28:
+        assert want == [6]
+    if r == 36:
+        assert want == [7]
+
+
 @pytest.mark.parametrize("r", list(range(1, 64)))
 def test_hcol_columns_are_exactly_the_empty_ones(r):
     # the kernel injects column L iff no zig-zag index < r lies in it (hcol_mask)
