@@ -570,6 +570,18 @@ __device__ __forceinline__ float2 compress_resid(const uint32_t (&Y)[8][8], cons
 #ifndef ADCT_RESID_HC
 #define ADCT_RESID_HC 1
 #endif
+#ifndef ADCT_RESID_P2
+#define ADCT_RESID_P2 1  // also inject the columns whose kept set is exactly {(0, L), (1, L)}
+#endif
+#ifndef ADCT_P2_LO
+#define ADCT_P2_LO 27  // measured per r (profiles/r02_variants_partial_injection.txt): +2-6 % at
+#endif                 // r = 27..35 (r = 28 +6 %), -3 % at r = 24 and -1 % at r = 36
+#ifndef ADCT_P2_HI
+#define ADCT_P2_HI 35
+#endif
+constexpr int resid_p2_mask(int R) {
+  return (ADCT_RESID_P2 && R >= ADCT_P2_LO && R <= ADCT_P2_HI) ? p2col_mask(R) : 0;
+}
 #ifndef ADCT_RESID_PC
 #define ADCT_RESID_PC 1  // also inject the columns whose only kept coefficient is (0, L) (pcol_mask)
 #endif
@@ -577,7 +589,8 @@ template <int R, int SM = 0>
 __device__ __forceinline__ float2 compress_resid_hc(const uint32_t (&Y)[8][8], const uint32_t (&H)[8][8],
                                                     const CompressParams& p) {
   constexpr int PC = ADCT_RESID_PC ? pcol_mask(R) : 0;
-  constexpr int RM = RESID + R, HC = hcol_mask(R) | PC;  // every injected column
+  constexpr int P2 = resid_p2_mask(R);
+  constexpr int RM = RESID + R, HC = hcol_mask(R) | PC | P2;  // every injected column
   static_assert(PC == 0 || SM != 2, "the bank-planned flavour injects only fully discarded columns");
   float2 V[64];
   static_for<64>([&](auto KLc) {
@@ -590,7 +603,19 @@ __device__ __forceinline__ float2 compress_resid_hc(const uint32_t (&Y)[8][8], c
   float2 UH[8][8];
   static_for<8>([&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
-    if constexpr ((PC >> L) & 1) {
+    if constexpr ((P2 >> L) & 1) {
+      // kept rows {0, 1}: W_0L (8 H - Y_0L) - T1[i] W_1L Y_1L, Y_1L = sum_i T1[i] H[i][L] (|.| <= 6120)
+      const uint32_t y0 = ((H[0][L] + H[1][L]) + (H[2][L] + H[3][L])) + ((H[4][L] + H[5][L]) + (H[6][L] + H[7][L]));
+      const uint32_t y1 = (H[0][L] + H[1][L] + H[2][L]) - (H[5][L] + H[6][L] + H[7][L]);
+      const uint32_t off = BIAS2 - y0;
+      constexpr float w0 = (float)(576 / (8 * dval(L))), w1 = (float)(576 / (6 * dval(L)));
+      const float2 v1 = f2fma(biased_pair(y1 + BIAS2), f2(w1), f2(-KF * w1));
+      static_for<8>([&](auto Ic) {
+        constexpr int i = decltype(Ic)::value;
+        const float2 u = f2fma(biased_pair((H[i][L] << 3) + off), f2(w0), f2(-KF * w0));
+        UH[L][i] = i < 3 ? f2sub(u, v1) : i > 4 ? f2add(u, v1) : u;
+      });
+    } else if constexpr ((PC >> L) & 1) {
       // only (0, L) kept: the discarded rows' column inverse is (576 / d_L) H[:, L] - W_0L Y_0L =
       // (W_0L) (8 H[i][L] - Y_0L) with W_0L = 576 / (8 d_L) an integer and Y_0L = sum_i H[i][L]:
       // 8 H - Y_0L is an exact int16 SWAR lane (|.| <= 32640), one LEA per row, then the same
@@ -929,9 +954,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB)
     uint32_t Y[8][8];
     float2 e2;
     if constexpr (RES) {
-      if constexpr (ADCT_RESID_HC && (hcol_mask(R) | (ADCT_RESID_PC ? pcol_mask(R) : 0)) != 0 && !GRP) {
+      constexpr int INJ = hcol_mask(R) | (ADCT_RESID_PC ? pcol_mask(R) : 0) | resid_p2_mask(R);
+      if constexpr (ADCT_RESID_HC && INJ != 0 && !GRP) {
         uint32_t H[8][8];
-        compress_fwd_h<RESID + R, hcol_mask(R) | (ADCT_RESID_PC ? pcol_mask(R) : 0), MIRB>(tile, lane, Y, H);
+        compress_fwd_h<RESID + R, INJ, MIRB>(tile, lane, Y, H);
         e2 = compress_resid_hc<R, SM>(Y, H, p);
       } else {
         compress_fwd<RESID + R, MODE, MIRB>(tile, lane, Y);

@@ -117,6 +117,22 @@ def test_row0_only_column_identity(L):
     assert 14 * (255 * max(T[L][T[L] > 0].sum(), -T[L][T[L] < 0].sum())) < 2 ** 15
 
 
+@pytest.mark.parametrize("L", list(range(1, 8)))
+def test_rows01_only_column_identity(L):
+    """compress_resid_hc's {0, 1}-kept injection (p2col_mask): for a column whose kept set is
+    {(0, L), (1, L)}, the discarded rows' column inverse is W_0L (8 H - (sum_i H_i) 1) -
+    W_1L (sum_i T1_i H_i) T1 with integer W_0L, W_1L, and sum_i T1_i H_i stays inside int16."""
+    T, W = EB.T, EB.W
+    d = np.diag(T @ T.T)
+    D = np.diag(W[:, L] * (np.arange(8) >= 2))            # discarded rows 2..7 of column L
+    lhs = T.T @ D @ T
+    one = np.ones(8, dtype=np.int64)
+    rhs = W[0, L] * (8 * np.eye(8, dtype=np.int64) - np.outer(one, one)) - W[1, L] * np.outer(T[1], T[1])
+    assert np.array_equal(lhs, rhs)
+    assert 576 // d[L] == 8 * W[0, L] and W[1, L] * 6 * d[L] == 576
+    assert 6 * 255 * max(T[L][T[L] > 0].sum(), -T[L][T[L] < 0].sum()) < 2 ** 15
+
+
 @pytest.mark.parametrize("r", list(range(23, 64)))
 def test_pcol_columns_are_the_row0_only_ones(r):
     M = np.array([[EB.zz(i, j) < r for j in range(8)] for i in range(8)])
